@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""bench.py -- headline benchmark: fp64 log I_v / log K_v evaluations per second.
+
+Workload (BASELINE.json configs[1] + configs[2]): per GPU, the paper's SciPy
+comparison grid -- v in {2^0..2^10}, 20M x per v uniform in [1, 100]
+(220M pairs, Fig. 1 caption).  One step = b200_log_iv_f64 over the
+whole grid followed by b200_log_kv_f64 over the same grid (440M evaluations).
+Inputs (3.5 GB) and outputs live in HBM, far larger than L2.
+
+Multi-GPU: one process per GPU (torchrun), every rank evaluates its own
+220M-pair batch (weak scaling, no data-path collective); time = max over ranks.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the oracle (oracle/, binary128 CPU) on bounded samples
+of the same workload -- the only reference this paper-only task has.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "logIv/logKv Gevals/s fp64"
+UNIT = "Gevals/s"
+N_PER_V = 20_000_000
+N_ORDERS = 11
+BYTES_PER_EVAL = 24          # read v, x (2 x 8 B), write out (8 B)  -- DESIGN.md §Roofline
+# FP64 operations per evaluation of the dominant kernel, from the ncu
+# instruction counts of the bench workload (profiles/).
+# None until measured: roofline then reports the HBM bound only.
+FP64_FLOP_PER_EVAL = {"log_iv": None, "log_kv": None}
+
+
+def _env_int(name, default):
+    try:
+        return int(os.environ.get(name, default))
+    except ValueError:
+        return default
+
+
+def _dist():
+    import torch.distributed as dist
+    ws = _env_int("WORLD_SIZE", 1)
+    if ws > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl")
+    return ws, _env_int("RANK", 0), _env_int("LOCAL_RANK", 0)
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except Exception:
+            self.p.kill()
+        self.f.flush()
+        self.f.seek(0)
+        sm, smax, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            c = [t.strip() for t in line.split(",")]
+            if len(c) < 9:
+                continue
+            try:
+                sm.append(float(c[1]))
+                smax = max(smax, float(c[2]))
+            except ValueError:
+                continue
+            for nm, val in zip(names, c[5:9]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def _peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("hbm_gbs", 6650.0), "measured"
+    return 6650.0, "fallback"
+
+
+def _fp64_peak():
+    p = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get("fp64_tflops"), d.get("source", "measured")
+    return None, None
+
+
+def cpu_baseline(target_s=12.0, seed=123):
+    """The oracle (as it stands) on host cores, bounded sample of the same workload."""
+    import numpy as np
+
+    import oracle
+    from paper_2409_08729_b200 import workloads
+    cores = os.cpu_count() or 1
+    n = 2000
+    done_evals, done_t = 0, 0.0
+    while True:
+        v, x = workloads.bench_grid_numpy(max(1, n // N_ORDERS), seed=seed + n)
+        t0 = time.perf_counter()
+        oracle.log_iv(v, x)
+        oracle.log_kv(v, x)
+        dt = time.perf_counter() - t0
+        done_evals += 2 * v.size
+        done_t += dt
+        if done_t >= target_s or n >= 50_000_000:
+            break
+        n = int(n * min(8.0, max(1.5, target_s / max(dt, 1e-3))))
+    return {"value": done_evals / done_t / 1e9, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{done_evals} evaluations (log I and log K on pairs drawn from the bench grid, "
+                      f"v-major, 11 orders), binary128 oracle, OpenMP over {cores} threads, {done_t:.1f} s"}
+
+
+def run_reference(args):
+    ws, rank, _ = _env_int("WORLD_SIZE", 1), _env_int("RANK", 0), 0
+    if rank != 0:
+        return
+    import oracle
+    from paper_2409_08729_b200 import workloads
+    cores = os.cpu_count() or 1
+    per_step = 20_000 * max(1, cores // 8)
+    ts = []
+    for s in range(args.warmup + args.steps):
+        v, x = workloads.bench_grid_numpy(max(1, per_step // (2 * N_ORDERS)), seed=1000 + s)
+        t0 = time.perf_counter()
+        oracle.log_iv(v, x)
+        oracle.log_kv(v, x)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            ts.append((2 * v.size, dt))
+    ev = sum(e for e, _ in ts)
+    tt = sum(t for _, t in ts)
+    val = ev / tt / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tt / len(ts),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f128",
+            "data": "synthetic",
+            "config": {"workload": "bench grid sample: v in {2^0..2^10}, x ~ U[1,100]; "
+                                   f"{ev // len(ts)} evals per step (bounded sample)"},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{ev // len(ts)} evaluations per step, binary128, OpenMP x{cores}"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2409_08729_b200 as B
+    from paper_2409_08729_b200 import workloads
+    ws, rank, lrank = _dist()
+    torch.cuda.set_device(lrank)
+    dev = torch.device("cuda", lrank)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+    n_per_v = args.n_per_v
+    v, x = workloads.bench_grid(n_per_v, seed=rank, device=dev)
+    n = v.numel()
+    out_i = torch.empty_like(v)
+    out_k = torch.empty_like(v)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(ev=None):
+        if ev is not None:
+            ev[0].record(stream)
+        B.log_iv(v, x, out=out_i)
+        if ev is not None:
+            ev[1].record(stream)
+        B.log_kv(v, x, out=out_k)
+        if ev is not None:
+            ev[2].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # non-finite guard on the warm-up outputs (the method never produces inf/NaN here)
+    nonfinite = int((~torch.isfinite(out_i)).sum().item() + (~torch.isfinite(out_k)).sum().item())
+
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    clocks = Clocks(lrank) if rank == 0 else None
+    time.sleep(0.3 if clocks else 0)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = B.launch_count()
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_start.record(stream)
+    for s in range(args.steps):
+        step(evs[s])
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    launches = B.launch_count() - launches0
+    clk = clocks.stop() if clocks else None
+    ms = t_start.elapsed_time(t_end)
+    ms_i = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
+    ms_k = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    evals_per_step = 2 * n * ws
+    value = evals_per_step * args.steps / (ms / 1e3) / 1e9
+
+    # ---- end to end through the C ABI with pinned HOST buffers (H2D + kernels + D2H timed)
+    e2e = None
+    if not args.skip_e2e:
+        vh = v.cpu().pin_memory()
+        xh = x.cpu().pin_memory()
+        oi = torch.empty_like(vh, pin_memory=True)
+        ok = torch.empty_like(vh, pin_memory=True)
+        B.log_iv_host(vh, xh, oi)
+        B.log_kv_host(vh, xh, ok)
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        reps = max(1, min(args.steps, 3))
+        for _ in range(reps):
+            B.log_iv_host(vh, xh, oi)
+            B.log_kv_host(vh, xh, ok)
+        te = time.perf_counter() - t0
+        if dist:
+            t = torch.tensor([te], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            te = float(t.item())
+        e2e = {"value": evals_per_step * reps / te / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": 2 * 2 * n * 8, "d2h_bytes_per_step": 2 * n * 8,
+               "note": "b200_log_iv_f64_host + b200_log_kv_f64_host on pinned host arrays; "
+                       "chunked H2D/kernel/D2H pipeline; host wall clock"}
+        del vh, xh, oi, ok
+
+    if rank != 0:
+        return
+    hbm_peak, hbm_src = _peaks()
+    dom, dom_ms = ("log_kv", ms_k) if ms_k >= ms_i else ("log_iv", ms_i)
+    gbs = BYTES_PER_EVAL * n / (dom_ms / 1e3) / 1e9
+    roof = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
+            "traffic": None, "kernel": f"bessel_eval_kernel ({dom})", "peak_source": hbm_src,
+            "kernel_ms": dom_ms}
+    fp64_peak, fp64_src = _fp64_peak()
+    fl = FP64_FLOP_PER_EVAL.get(dom)
+    if fl and fp64_peak:
+        tf = fl * n / (dom_ms / 1e3) / 1e12
+        if tf / fp64_peak > gbs / hbm_peak:
+            roof = {"bound": "alu", "achieved": tf, "peak": fp64_peak, "unit": "TFLOP/s",
+                    "frac": tf / fp64_peak, "traffic": None, "kernel": f"bessel_eval_kernel ({dom})",
+                    "peak_source": fp64_src, "kernel_ms": dom_ms, "fp64_flop_per_eval": fl,
+                    "hbm_frac": gbs / hbm_peak}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"log I_v and log K_v over v in {{2^0..2^10}} x {n_per_v} x~U[1,100] per GPU "
+                               f"({n} pairs, v-major; configs[1]+configs[2])",
+                   "pairs_per_gpu": n, "evals_per_step": evals_per_step,
+                   "l2": "inputs_larger_than_l2 (3.5 GB in, 3.5 GB out per step)",
+                   "parallelism": f"dp{ws} (contiguous batch per rank, no collective)"},
+        "kernel_ms": {"log_iv": ms_i, "log_kv": ms_k},
+        "roofline": roof,
+        "gpu_launches": launches,
+        "nonfinite_outputs": nonfinite,
+        "e2e": e2e,
+        "clocks": clk,
+    }
+    if not args.skip_cpu_baseline and ws == 1:
+        line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n-per-v", type=int, default=N_PER_V)
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+    try:
+        import torch.distributed as dist
+        if dist.is_initialized():
+            dist.destroy_process_group()
+    except Exception:
+        pass
+
+
+if __name__ == "__main__":
+    main()

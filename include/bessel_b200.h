@@ -1,0 +1,127 @@
+/*
+ * bessel_b200.h -- C ABI of the B200-native hot path of arXiv 2409.08729
+ * ("Robust and efficient computation of the logarithm of modified Bessel
+ * functions", PAPER.md).  Shared library: libbessel_b200.so (sm_100a).
+ *
+ * Conventions for every entry point
+ *   - Pointers named *_d are DEVICE pointers (cudaMalloc / torch CUDA
+ *     tensors), pointers named *_h are HOST pointers (pinned recommended).
+ *     The library never takes ownership; the caller allocates and frees.
+ *   - Arrays are dense, contiguous, element i of every array belongs to the
+ *     same (v_i, x_i) pair.  n may be 0 (no-op, returns B200_OK).
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Device
+ *     calls are asynchronous w.r.t. the host; host-buffer (_h) calls return
+ *     after the results are in the host buffer.
+ *   - Return value: 0 (B200_OK) on success, otherwise a b200_status code;
+ *     b200_last_error() returns a static string describing the last failure.
+ *     Invalid arguments (n < 0, NULL pointer with n > 0) are rejected before
+ *     any launch.  Out-of-domain inputs are NOT errors: they produce NaN in
+ *     that element only (see each function).
+ */
+#ifndef BESSEL_B200_H
+#define BESSEL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    B200_OK = 0,
+    B200_ERR_INVALID_ARGUMENT = 1,
+    B200_ERR_CUDA = 2,
+    B200_ERR_NO_DEVICE = 3
+} b200_status;
+
+/* Region ids written by b200_classify_* (Algorithm 1, PAPER.md lines 359-386,
+ * GPU branch set {mu, U13, fallback} per the Algorithm 1 caption). */
+enum {
+    B200_METHOD_MU = 0,        /* large-argument expansion, Eqs. (log Iv mu k)/(log Kv mu k) */
+    B200_METHOD_U13 = 1,       /* uniform large-order (Debye) expansion, Eqs. (log Iv u k)/(log Kv u k) */
+    B200_METHOD_FALLBACK = 2   /* I: log-domain power series, Eq. (log Iv); K: small-argument method */
+};
+
+/* ------------------------------------------------------------------------
+ * log I_v(x) -- PAPER.md §3.1 (Eq. (Iv infinite series), line 127) evaluated by
+ * Algorithm 1 (lines 359-386) on the GPU branch set.
+ *   v_d, x_d : n orders / arguments.  Domain v >= 0, x >= 0 (paper line 125).
+ *   out_d    : n results, log I_v(x).  log I_0(0) = 0; log I_v(0) = -inf (v>0);
+ *              NaN where v < 0, x < 0 or an input is NaN.
+ * Accuracy (f64): |out - exact| <= 1e-13 * max(|exact|, 1) on the tested
+ * domain; f32: 1e-5.
+ */
+int b200_log_iv_f64(const double *v_d, const double *x_d, double *out_d, int64_t n, void *stream);
+int b200_log_iv_f32(const float *v_d, const float *x_d, float *out_d, int64_t n, void *stream);
+
+/* ------------------------------------------------------------------------
+ * log K_v(x) -- PAPER.md §3.2 (Eqs. (log Kv mu k), (log Kv u k), lines 233-246)
+ * by Algorithm 1; the small-argument fallback replaces the paper's Simpson
+ * integral (line 251-269) by Temme's method, see DESIGN.md §K-fallback.
+ *   Domain: x > 0, any real v (K_{-v} = K_v).  x = 0 -> +inf (pole);
+ *   x < 0 or NaN input -> NaN.
+ */
+int b200_log_kv_f64(const double *v_d, const double *x_d, double *out_d, int64_t n, void *stream);
+int b200_log_kv_f32(const float *v_d, const float *x_d, float *out_d, int64_t n, void *stream);
+
+/* The paper's own K fallback (log-domain Rothwell integral, Simpson N=600,
+ * heuristic maxima) on the same dispatch -- kept for
+ * fidelity studies; accuracy is the paper's (~1e-9, Table 2), not 1e-13. */
+int b200_log_kv_paper_f64(const double *v_d, const double *x_d, double *out_d, int64_t n, void *stream);
+
+/* Region id (B200_METHOD_*) per element, as int8 -- the dispatch of
+ * Algorithm 1 / Table 1 (lines 338-352) with the GPU branch set. */
+int b200_classify_f64(const double *v_d, const double *x_d, int8_t *method_d, int64_t n, void *stream);
+
+/* ------------------------------------------------------------------------
+ * Host-buffer variants (end-to-end): v_h, x_h, out_h are HOST arrays; the
+ * library stages them through device memory in chunks, overlapping
+ * H2D copy / kernel / D2H copy on internal streams.  Blocking.
+ */
+int b200_log_iv_f64_host(const double *v_h, const double *x_h, double *out_h, int64_t n);
+int b200_log_kv_f64_host(const double *v_h, const double *x_h, double *out_h, int64_t n);
+
+/* ------------------------------------------------------------------------
+ * von Mises-Fisher fit, §6.3 (lines 663-693).
+ *
+ * b200_vmf_colsum_*: colsum_d[j] (+)= sum_i X[i, j] over the n rows of the
+ *   row-major n x d matrix X_d (leading dimension ld >= d elements), fp64
+ *   accumulation.  If accumulate == 0 colsum_d is overwritten, else added to.
+ *   This is the data-parallel part (Eq. (mean direction estimate), line 672);
+ *   with rows sharded over GPUs the caller all-reduces colsum_d.
+ *
+ * b200_vmf_fit_from_colsum: given the global column sum (d doubles) and the
+ *   global row count n_total, computes on the device
+ *     mu_d[0..d)   = xbar / Rbar                      (line 672)
+ *     stats_d[0]   = Rbar
+ *     stats_d[1..3]= kappa0, kappa1, kappa2            (Eq. (kappa estimates), lines 676-680)
+ *     stats_d[4]   = kappa_mle  (root of Rbar - A_p(kappa), the maximiser of
+ *                                the log-likelihood, lines 684-691)
+ *     stats_d[5]   = logLik(kappa_mle)                 (lines 685-689)
+ *     stats_d[6]   = A_p(kappa_mle) - Rbar  (stationarity residual)
+ *     stats_d[7]   = number of MLE iterations
+ *   stats_d must hold 8 doubles.  p = d.  Rbar outside (0,1) -> stats NaN.
+ *
+ * b200_vmf_fit_*: both steps on one device (workspace: d doubles, device).
+ */
+int b200_vmf_colsum_f32(const float *X_d, int64_t n, int64_t d, int64_t ld, double *colsum_d,
+                        int accumulate, void *stream);
+int b200_vmf_colsum_f64(const double *X_d, int64_t n, int64_t d, int64_t ld, double *colsum_d,
+                        int accumulate, void *stream);
+int b200_vmf_fit_from_colsum(const double *colsum_d, int64_t n_total, int64_t d, double *mu_d,
+                             double *stats_d, void *stream);
+int b200_vmf_fit_f32(const float *X_d, int64_t n, int64_t d, double *workspace_d, double *mu_d,
+                     double *stats_d, void *stream);
+int b200_vmf_fit_f64(const double *X_d, int64_t n, int64_t d, double *workspace_d, double *mu_d,
+                     double *stats_d, void *stream);
+
+/* ------------------------------------------------------------------------ */
+const char *b200_last_error(void);
+/* Number of kernel launches issued by this library since load (diagnostic;
+ * bench.py reports it as gpu_launches). */
+int64_t b200_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BESSEL_B200_H */

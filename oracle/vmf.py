@@ -42,6 +42,14 @@ def mean_direction(X):
     return xbar / rbar, rbar, xbar
 
 
+def mean_resultant_rows(X):
+    """Rbar for a large sample: column sums in float64 by numpy's pairwise summation
+    (a library primitive; used where math.fsum over every column is too slow)."""
+    X = np.asarray(X)
+    xbar = np.sum(X, axis=0, dtype=np.float64) / X.shape[0]
+    return math.sqrt(math.fsum((xbar * xbar).tolist()))
+
+
 def a_p(p, kappa):
     """A_p(kappa) = I_{p/2}(kappa)/I_{p/2-1}(kappa) (line 677), from binary128 logs."""
     kappa = float(kappa)

@@ -1,0 +1,339 @@
+// bessel_math.cuh -- per-element device math for log I_v(x) / log K_v(x).
+//
+// PAPER.md = arXiv 2409.08729.  Every function cites the passage it follows.
+// Templated on the arithmetic type T (double for the f64 path, float for the
+// f32 path).  Nothing here allocates, synchronises or touches global memory.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include "tables.h"
+
+namespace b200 {
+
+// ---------------------------------------------------------------- constants
+static __constant__ double c_uk_d[B200_UK_NCOEF] = B200_UK_TABLE_INIT;
+static __constant__ float c_uk_f[B200_UK_NCOEF] = B200_UK_TABLE_INIT;
+static __constant__ double c_rg_d[B200_RGAMMA_NT] = B200_RGAMMA_INIT;
+static __constant__ float c_rg_f[B200_RGAMMA_NT] = B200_RGAMMA_INIT;
+
+template <typename T> struct Tr;
+template <> struct Tr<double> {
+    static constexpr double eps = 1.1102230246251565e-16;   // 2^-53
+    static constexpr int rg_terms = 28;
+    __device__ static double uk(int i) { return c_uk_d[i]; }
+    __device__ static double rg(int i) { return c_rg_d[i]; }
+};
+template <> struct Tr<float> {
+    static constexpr float eps = 5.9604645e-08f;             // 2^-24
+    static constexpr int rg_terms = 12;
+    __device__ static float uk(int i) { return c_uk_f[i]; }
+    __device__ static float rg(int i) { return c_rg_f[i]; }
+};
+
+// Overload helpers so templates pick the right precision.
+__device__ __forceinline__ double d_rsqrt(double a) { return rsqrt(a); }
+__device__ __forceinline__ float d_rsqrt(float a) { return rsqrtf(a); }
+__device__ __forceinline__ double d_sinpi(double a) { return sinpi(a); }
+__device__ __forceinline__ float d_sinpi(float a) { return sinpif(a); }
+__device__ __forceinline__ double d_lgamma(double a) { return lgamma(a); }
+__device__ __forceinline__ float d_lgamma(float a) { return lgammaf(a); }
+__device__ __forceinline__ double d_rcp(double a) { return 1.0 / a; }
+__device__ __forceinline__ float d_rcp(float a) { return __frcp_rn(a); }
+
+// ---------------------------------------------------------------- dispatch
+// Algorithm 1 / Table 1 (lines 338-352), with the
+// GPU branch set: "When running on a GPU the branches for the mu_3, U_4, U_6,
+// U_9 expressions are removed" (line 384).  Predicates read as strict
+// inequalities with natural logarithms (reading R3).  Logs are
+// always taken in double so the f32 and f64 paths dispatch identically.
+enum : int { M_MU = 0, M_U13 = 1, M_FALLBACK = 2 };
+
+__device__ __forceinline__ int select_method(double v, double x) {
+    bool mu = (x > 30.0) && (v < 15.3919);
+    if (!mu && x > 59.6925) mu = (0.5113 * log(x) + 0.7939 > log(v));
+    if (mu) return M_MU;
+    if ((x > 19.6931 && v > 0.7) || v > 12.6964) return M_U13;
+    return M_FALLBACK;
+}
+
+// Number of terms of the mu_K expansion.  The paper uses K = 20 (Table 1);
+// we run the same recurrence to K = 26 so the truncation error stays below
+// fp64 resolution on the whole region (reading R5).
+constexpr int KMU = 26;
+
+// ---------------------------------------------------------------- mu_K
+// Eq. (log Iv mu k) (line 203-205) / Eq. (log Kv mu k) (line 234-236):
+//   log I ~ x - 1/2 log(2 pi x) + log|1 + sum_k (-1)^k prod_{j<=k}(mu-(2j-1)^2) / (k! (8x)^k)|
+//   log K ~ 1/2 (log pi - log 2x) - x + log|1 + sum_k prod_{j<=k}(mu-(2j-1)^2) / (k! (8x)^k)|
+// mu = 4 v^2.  The sum is evaluated in nested (Horner) form
+//   1 + r_1 (1 + r_2 (1 + ... r_K)),  r_k = s (mu - (2k-1)^2) / (8 x k),
+// which is the paper's term recurrence ("the terms in the series can also be
+// calculated recursively", line 208) read from the innermost term outwards.
+template <typename T, bool IS_K>
+__device__ __forceinline__ T mu_series(T v, T x) {
+    const T mu = T(4) * v * v;
+    const T c = (IS_K ? T(1) : T(-1)) / (T(8) * x);
+    T s = T(1);
+#pragma unroll
+    for (int k = KMU; k >= 1; --k) {
+        const T a = mu - T((2 * k - 1) * (2 * k - 1));
+        const T r = a * (c * T(1.0 / k));
+        s = fma(r, s, T(1));
+    }
+    return fabs(s);
+}
+
+template <typename T>
+__device__ __forceinline__ T log_iv_mu(T v, T x) {
+    // x - 1/2 log(2 pi x) + log|S|  =  x + log(|S| / sqrt(2 pi x))
+    const T S = mu_series<T, false>(v, x);
+    return x + log(S * d_rsqrt(T(2.0 * CUDART_PI) * x));
+}
+
+template <typename T>
+__device__ __forceinline__ T log_kv_mu(T v, T x) {
+    // 1/2 (log pi - log 2x) - x + log|S|  =  -x + log(|S| sqrt(pi / 2x))
+    const T S = mu_series<T, true>(v, x);
+    return -x + log(S * d_rsqrt(T(2.0 / CUDART_PI) * x));
+}
+
+// ---------------------------------------------------------------- U_13
+// Eq. (log Iv u k) (lines 211-215) / Eq. (log Kv u k) (lines 241-245):
+//   x' = x/v, t = 1/sqrt(1+x'^2), eta = sqrt(1+x'^2) + log(x'/(1+sqrt(1+x'^2)))
+//   log I ~ -1/2 log(2 pi v) + v eta - 1/4 log(1+x'^2) + log|1 + sum_k u_k(t)/v^k|
+//   log K ~  1/2 log(pi/(2v)) - v eta - 1/4 log(1+x'^2) + log|1 + sum_k (-1)^k u_k(t)/v^k|
+// u_k(t) = t^k P_k(t^2) (tables.h, generated from Eqs. (u0),(uk)).  With
+// w = +-t/v the sum is w (P_1 + w (P_2 + ... + w P_13)).
+template <typename T>
+__device__ __forceinline__ T uk_row(int k, T t2) {
+    // P_k(t2) by Horner, k+1 coefficients starting at UK_OFF[k]
+    const int off = (k * (k + 1)) / 2;
+    T p = Tr<T>::uk(off + k);
+#pragma unroll
+    for (int j = k - 1; j >= 0; --j) p = fma(p, t2, Tr<T>::uk(off + j));
+    return p;
+}
+
+template <typename T, bool IS_K>
+__device__ __forceinline__ T log_bessel_u13(T v, T x) {
+    const T z = x / v;
+    const T r2 = fma(z, z, T(1));
+    const T r = sqrt(r2);
+    const T t = d_rcp(r);
+    const T t2 = t * t;
+    const T w = (IS_K ? -t : t) / v;
+    T acc = uk_row<T>(13, t2);
+#pragma unroll
+    for (int k = 12; k >= 1; --k) acc = fma(acc, w, uk_row<T>(k, t2));
+    const T S = fabs(fma(acc, w, T(1)));
+    const T eta = r + log(z / (T(1) + r));
+    if (!IS_K) {
+        // -1/2 log(2 pi v) - 1/4 log(1+x'^2) + log|S| = log(|S| / sqrt(2 pi v r))
+        return v * eta + log(S * d_rsqrt(T(2.0 * CUDART_PI) * v * r));
+    } else {
+        // 1/2 log(pi/(2v)) - 1/4 log(1+x'^2) + log|S| = log(|S| sqrt(pi/(2 v r)))
+        return -v * eta + log(S * d_rsqrt(T(2.0 / CUDART_PI) * v * r));
+    }
+}
+
+// ---------------------------------------------------------------- series (I)
+// Eq. (Iv infinite series) (line 127) with the recurrence Eqs. (ak recurrence
+// base)/(ak recurrence) (lines 148-150) and the logarithm-of-a-sum form
+// Eq. (log Iv) (lines 153-155):
+//   log I = v log(x/2) + log a_0 + log sum_k (a_k / a_0),  log a_0 = -lgamma(v+1).
+// The ratios a_k/a_0 are carried in linear scale (b_{k+1} = b_k x^2 / (4(k+1)(k+v+1))):
+// in the fallback region x <= 30, so sum_k b_k <= Gamma(v+1) e^x < 1e23 and
+// nothing can overflow; pivoting the log-sum-exp on a_0 instead of the peak
+// a_K (line 120) is therefore exact up to rounding (reading R6).
+// Stop once past the peak term (Eq. (K)) and the term is below eps
+// of the partial sum ("Terms less than machine precision, relative to the
+// maximum value, are ignored", line 194).
+template <typename T>
+__device__ __forceinline__ T log_iv_series(T v, T x) {
+    if (x == T(0)) return v == T(0) ? T(0) : T(-CUDART_INF);
+    const T q = T(0.25) * x * x;
+    T b = T(1), S = T(1);
+    for (int k = 0; k < 200; ++k) {
+        const T d = (T(k) + T(1)) * (T(k) + v + T(1));
+        b = b * q / d;
+        S += b;
+        if (d > q && b <= S * Tr<T>::eps) break;
+    }
+    return v * log(T(0.5) * x) - d_lgamma(v + T(1)) + log(S);
+}
+
+// ---------------------------------------------------------------- K fallback
+// Small-argument region of K (x <= 30, v <= 12.7 after dispatch).  The paper
+// evaluates Eq. (log Kv integral) with Simpson N = 600 (lines 248-324); its
+// measured error against the binary128 oracle is up to 5.7e-10 (DESIGN.md
+// §K-fallback), above the 1e-13 target.  We use Temme's method instead:
+// K_mu, K_{mu+1} for |mu| <= 1/2 by Temme's series (x <= 2) or Steed's
+// continued fraction CF2 (x > 2), then the forward recurrence
+// K_{nu+1} = K_{nu-1} + (2 nu / x) K_nu (stable for K) up to nu = v, with the
+// running value kept as mantissa * 2^e so nothing overflows; the result is
+// returned as a logarithm.
+template <typename T>
+__device__ __forceinline__ void temme_gammas(T mu, T &gam1, T &gam2, T &gampl, T &gammi) {
+    // 1/Gamma(1+z) = sum_j c_j z^j  (tables.h).  Even/odd parts give
+    // gam2 = (1/G(1-mu) + 1/G(1+mu))/2 = sum_even c_j mu^j
+    // gam1 = (1/G(1-mu) - 1/G(1+mu))/(2 mu) = -sum_odd c_j mu^(j-1)
+    const T m2 = mu * mu;
+    const int N = Tr<T>::rg_terms;
+    T ev = Tr<T>::rg(N - 2), od = Tr<T>::rg(N - 1);
+#pragma unroll
+    for (int j = N - 4; j >= 0; j -= 2) {
+        ev = fma(ev, m2, Tr<T>::rg(j));
+        od = fma(od, m2, Tr<T>::rg(j + 1));
+    }
+    gam2 = ev;
+    gam1 = -od;
+    gampl = ev + mu * od;   // 1/Gamma(1+mu)
+    gammi = ev - mu * od;   // 1/Gamma(1-mu)
+}
+
+// returns log K_mu(x) and rho = K_{mu+1}(x) / K_mu(x)
+template <typename T>
+__device__ __forceinline__ T temme_kmu(T mu, T x, T &rho) {
+    const T eps = Tr<T>::eps;
+    if (x <= T(2)) {
+        const T d = -log(T(0.5) * x);       // ln(2/x)
+        const T e = mu * d;
+        const T fact = (mu == T(0)) ? T(1) : (T(CUDART_PI) * mu) / d_sinpi(mu);
+        const T fact2 = (e == T(0)) ? T(1) : sinh(e) / e;
+        T gam1, gam2, gampl, gammi;
+        temme_gammas<T>(mu, gam1, gam2, gampl, gammi);
+        T ff = fact * (gam1 * cosh(e) + gam2 * fact2 * d);
+        T sum = ff;
+        const T ee = exp(e);
+        T p = T(0.5) * ee / gampl;          // 1/2 (2/x)^mu Gamma(1+mu)
+        T q = T(0.5) / (ee * gammi);        // 1/2 (x/2)^mu Gamma(1-mu)
+        T c = T(1);
+        const T dd = T(0.25) * x * x;
+        T sum1 = p;
+        const T m2 = mu * mu;
+        for (int i = 1; i < 100; ++i) {
+            const T fi = T(i);
+            ff = (fi * ff + p + q) / (fi * fi - m2);
+            c *= dd / fi;
+            p /= (fi - mu);
+            q /= (fi + mu);
+            const T del = c * ff;
+            sum += del;
+            sum1 += c * (p - fi * ff);
+            if (fabs(del) < fabs(sum) * eps) break;
+        }
+        rho = (T(2) / x) * (sum1 / sum);
+        return log(sum);
+    } else {
+        const T m2 = mu * mu;
+        T b = T(2) * (T(1) + x);
+        T d = T(1) / b;
+        T h = d, delh = d;
+        T q1 = T(0), q2 = T(1);
+        const T a1 = T(0.25) - m2;
+        T q = a1, c = a1;
+        T a = -a1;
+        T s = T(1) + q * delh;
+        for (int i = 1; i < 400; ++i) {
+            const T fi = T(i);
+            a -= T(2 * i);
+            c = -a * c / (fi + T(1));
+            const T qnew = (q1 - b * q2) / a;
+            q1 = q2;
+            q2 = qnew;
+            q += c * qnew;
+            b += T(2);
+            d = T(1) / (b + a * d);
+            delh = (b * d - T(1)) * delh;
+            h += delh;
+            const T dels = q * delh;
+            s += dels;
+            if (fabs(dels) < fabs(s) * eps) break;
+        }
+        h = a1 * h;
+        rho = (mu + x + T(0.5) - h) / x;
+        // K_mu = sqrt(pi/(2x)) e^{-x} / s
+        return -x - log(s * d_rsqrt(T(CUDART_PI / 2.0) / x));
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ T log_kv_fallback(T v, T x) {
+    const int nl = int(floor(v + T(0.5)));
+    const T mu = v - T(nl);
+    T rho;
+    const T lk = temme_kmu<T>(mu, x, rho);
+    if (nl == 0) return lk;
+    // forward recurrence on K_{mu+i} / K_mu, scaled by 2^-e
+    T km = T(1), kp = rho;
+    const T two_over_x = T(2) / x;
+    int e = 0;
+    for (int i = 1; i <= nl; ++i) {
+        const T kn = fma((mu + T(i)) * two_over_x, kp, km);
+        km = kp;
+        kp = kn;
+        if (kp > T(1e30)) { km *= T(1e-30); kp *= T(1e-30); e += 1; }
+    }
+    // after nl steps km = K_v / K_mu * 1e-30^e
+    return lk + log(km) + T(e) * T(69.07755278982137);   // 30 ln 10
+}
+
+// ---------------------------------------------------------------- paper K
+// The paper's own small-argument K method (kept for fidelity studies):
+// Eq. (log Kv integral) (lines 251-254), n = 8, beta = 2n/(2v+1),
+//   log K = 1/2 log pi - lgamma(v+1/2) - v log(2x) - x + log int_0^1 (g + h) du,
+// Simpson's 1/3 rule with N = 600 (line 269) and weights w_k (lines 272-275),
+// each of G and H summed in log scale around the heuristic maxima u_g* = 1,
+// u_h* = 1/2 (v < 2) or 1/(2v) (lines 305, 318-323).  The Simpson prefactor is
+// h/3 = 1/(3N) (the printed 1/(6N), line 265-267, is read as a typo:
+// DESIGN.md reading R7).  Only v >= 0 reaches here (|v| taken by the caller).
+template <typename T>
+__device__ __forceinline__ T log_kv_integral_paper(T v, T x) {
+    const int N = 600;
+    const T n = T(8);
+    const T beta = T(2) * n / (T(2) * v + T(1));
+    const T lbeta = log(beta);
+    const T vm = v - T(0.5);
+    const T twox = T(2) * x;
+    // log g(u) = log beta - u^beta + (v-1/2) log(2x + u^beta) + (n-1) log u
+    // log h(u) = -1/u - (2v+1) log u + (v-1/2) log(2xu + 1)
+    const T lg_max = lbeta - T(1) + vm * log(twox + T(1));          // g at u* = 1
+    const T uh = (v < T(2)) ? T(0.5) : T(0.5) / v;
+    const T lh_max = -T(1) / uh - (T(2) * v + T(1)) * log(uh) + vm * log1p(twox * uh);
+    T G = T(0), H = T(0);
+    for (int k = 1; k <= N; ++k) {
+        const T u = T(k) / T(N);
+        const T w = (k == N) ? T(1) : ((k & 1) ? T(4) : T(2));
+        const T lu = log(u);
+        const T ub = exp(beta * lu);
+        const T lg = lbeta - ub + vm * log(twox + ub) + (n - T(1)) * lu;
+        const T lh = -T(1) / u - (T(2) * v + T(1)) * lu + vm * log1p(twox * u);
+        G += w * exp(lg - lg_max);
+        H += w * exp(lh - lh_max);
+    }
+    const T lG = lg_max + log(G), lH = lh_max + log(H);
+    const T M = fmax(lG, lH);
+    const T lint = -log(T(3 * N)) + M + log(exp(lG - M) + exp(lH - M));
+    return T(0.5) * T(1.1447298858494002) - d_lgamma(v + T(0.5)) - v * log(twox) - x + lint;
+}
+
+// ---------------------------------------------------------------- entry points
+template <typename T>
+__device__ __forceinline__ T log_iv_method(int m, T v, T x) {
+    if (m == M_MU) return log_iv_mu<T>(v, x);
+    if (m == M_U13) return log_bessel_u13<T, false>(v, x);
+    return log_iv_series<T>(v, x);
+}
+
+template <typename T, bool PAPER>
+__device__ __forceinline__ T log_kv_method(int m, T v, T x) {
+    if (m == M_MU) return log_kv_mu<T>(v, x);
+    if (m == M_U13) return log_bessel_u13<T, true>(v, x);
+    if (PAPER) return log_kv_integral_paper<T>(v, x);
+    return log_kv_fallback<T>(v, x);
+}
+
+}  // namespace b200

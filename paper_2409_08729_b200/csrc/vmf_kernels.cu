@@ -1,0 +1,291 @@
+// vmf_kernels.cu -- von Mises-Fisher fit (§6.3).
+//
+// Data-parallel part: the column sum of the n x d feature matrix (the mean
+// x̄ of Eq. (mean direction estimate), line 672) -- an HBM-bound streaming
+// reduction, two deterministic stages (per-row-slab partials, then a fixed
+// order sum over slabs).  Scalar part: Rbar, mu, kappa0/1/2 (Eq. (kappa
+// estimates), lines 676-680) and the MLE of kappa (lines 684-691) run in one
+// CTA on the device with the same log I_v device code as the batch kernels.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <atomic>
+#include <mutex>
+
+#include "../../include/bessel_b200.h"
+#include "bessel_math.cuh"
+
+namespace b200 {
+
+extern std::atomic<int64_t> g_launches;   // defined in bessel_kernels.cu
+
+constexpr int CS_TPB = 256;
+
+template <typename T> struct VecOf;
+template <> struct VecOf<float> { using V = float4; static constexpr int N = 4; };
+template <> struct VecOf<double> { using V = double2; static constexpr int N = 2; };
+
+__device__ __forceinline__ void vadd(double *acc, const float4 &a) {
+    acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+}
+__device__ __forceinline__ void vadd(double *acc, const double2 &a) {
+    acc[0] += a.x; acc[1] += a.y;
+}
+
+// Stage 1: CTA (bx, by) sums rows [by*rows_per, (by+1)*rows_per) of the
+// column slab [bx*CW, bx*CW + CW).  Each thread owns VN consecutive columns
+// and streams its rows with VN-wide loads (a warp reads 32*VN*sizeof(T)
+// contiguous bytes per row); 4 rows in flight per thread.
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(CS_TPB) colsum_partial_kernel(const T *__restrict__ X, int64_t n, int64_t d,
+                                                                int64_t ld, int64_t rows_per,
+                                                                double *__restrict__ part) {
+    constexpr int VN = VEC ? VecOf<T>::N : 1;
+    constexpr int CW = CS_TPB * VN;
+    const int64_t c0 = int64_t(blockIdx.x) * CW + int64_t(threadIdx.x) * VN;
+    const int64_t r0 = int64_t(blockIdx.y) * rows_per;
+    int64_t r1 = r0 + rows_per;
+    if (r1 > n) r1 = n;
+    double acc[VN];
+#pragma unroll
+    for (int j = 0; j < VN; ++j) acc[j] = 0.0;
+    if (c0 < d) {
+        if (VEC && c0 + VN <= d) {
+            using V = typename VecOf<T>::V;
+            const T *p = X + r0 * ld + c0;
+            int64_t r = r0;
+            for (; r + 4 <= r1; r += 4) {
+                V a0 = __ldcs(reinterpret_cast<const V *>(p));
+                V a1 = __ldcs(reinterpret_cast<const V *>(p + ld));
+                V a2 = __ldcs(reinterpret_cast<const V *>(p + 2 * ld));
+                V a3 = __ldcs(reinterpret_cast<const V *>(p + 3 * ld));
+                vadd(acc, a0); vadd(acc, a1); vadd(acc, a2); vadd(acc, a3);
+                p += 4 * ld;
+            }
+            for (; r < r1; ++r, p += ld) vadd(acc, __ldcs(reinterpret_cast<const V *>(p)));
+        } else {
+            for (int j = 0; j < VN; ++j) {
+                if (c0 + j >= d) break;
+                const T *p = X + r0 * ld + c0 + j;
+                double a = 0.0;
+                for (int64_t r = r0; r < r1; ++r, p += ld) a += double(*p);
+                acc[j] = a;
+            }
+        }
+        double *o = part + int64_t(blockIdx.y) * d + c0;
+#pragma unroll
+        for (int j = 0; j < VN; ++j)
+            if (c0 + j < d) o[j] = acc[j];
+    }
+}
+
+// Stage 2: colsum[j] (+)= sum_s part[s*d + j], slabs in fixed order.
+__global__ void colsum_reduce_kernel(const double *__restrict__ part, int64_t nslab, int64_t d,
+                                     double *__restrict__ colsum, int accumulate) {
+    for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < d; j += int64_t(gridDim.x) * blockDim.x) {
+        double s = 0.0;
+        for (int64_t k = 0; k < nslab; ++k) s += part[k * d + j];
+        colsum[j] = accumulate ? colsum[j] + s : s;
+    }
+}
+
+// ---------------------------------------------------------------- scalar part
+__device__ double log_iv_scalar(double v, double x) {
+    if (x == 0.0) return v == 0.0 ? 0.0 : -CUDART_INF;
+    return log_iv_method<double>(select_method(v, x), v, x);
+}
+
+// A_p(kappa) = I_{p/2}(kappa) / I_{p/2-1}(kappa)  (line 677)
+__device__ double a_p(double p, double kappa) {
+    if (kappa <= 0.0) return 0.0;
+    return exp(log_iv_scalar(0.5 * p, kappa) - log_iv_scalar(0.5 * p - 1.0, kappa));
+}
+
+// F(kappa) of Eq. (kappa estimates)
+__device__ double newton_F(double p, double rbar, double k) {
+    const double A = a_p(p, k);
+    return k - (A - rbar) / (1.0 - A * A - (p - 1.0) / k * A);
+}
+
+constexpr int FIT_TPB = 1024;
+
+__global__ void __launch_bounds__(FIT_TPB) vmf_fit_kernel(const double *__restrict__ colsum, int64_t n_total,
+                                                          int64_t d, double *__restrict__ mu,
+                                                          double *__restrict__ stats) {
+    __shared__ double s_red[FIT_TPB / 32];
+    __shared__ double s_rbar;
+    const double inv_n = 1.0 / double(n_total);
+    double loc = 0.0;
+    for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
+        const double m = colsum[j] * inv_n;
+        loc = fma(m, m, loc);
+    }
+    // warp-shuffle reduction of ||xbar||^2, then across warps
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) loc += __shfl_xor_sync(0xffffffffu, loc, o);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = loc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double w = threadIdx.x < (blockDim.x >> 5) ? s_red[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+        if (threadIdx.x == 0) s_rbar = sqrt(w);
+    }
+    __syncthreads();
+    const double rbar = s_rbar;
+    for (int64_t j = threadIdx.x; j < d; j += blockDim.x) mu[j] = colsum[j] * inv_n / rbar;
+    if (threadIdx.x != 0) return;
+
+    const double p = double(d);
+    stats[0] = rbar;
+    if (!(rbar > 0.0 && rbar < 1.0)) {
+        for (int i = 1; i < 8; ++i) stats[i] = CUDART_NAN;
+        return;
+    }
+    // Eq. (kappa estimates)
+    const double k0 = rbar * (p - rbar * rbar) / (1.0 - rbar * rbar);
+    const double k1 = newton_F(p, rbar, k0);
+    const double k2 = newton_F(p, rbar, k1);
+    stats[1] = k0;
+    stats[2] = k1;
+    stats[3] = k2;
+    // MLE: d logLik/dkappa = Rbar - A_p(kappa) (A_p strictly increasing), so
+    // the maximiser is the root; safeguarded Newton from kappa2 with a
+    // bracket [lo, hi] (lo: A < Rbar, hi: A > Rbar), bisection fallback.
+    double lo = 0.0, hi = CUDART_INF;
+    double k = (k2 > 0.0 && isfinite(k2)) ? k2 : k0;
+    int it = 0;
+    for (; it < 100; ++it) {
+        const double A = a_p(p, k);
+        const double g = A - rbar;
+        if (g == 0.0) break;
+        if (g < 0.0) lo = k; else hi = k;
+        const double dA = 1.0 - A * A - (p - 1.0) / k * A;
+        double kn = k - g / dA;
+        if (!(kn > lo && kn < hi) || !isfinite(kn)) kn = isfinite(hi) ? 0.5 * (lo + hi) : 2.0 * k;
+        const double step = fabs(kn - k);
+        k = kn;
+        if (step <= 4e-16 * k) { ++it; break; }
+        if (isfinite(hi) && (hi - lo) <= 4e-16 * hi) { ++it; break; }
+    }
+    const double A = a_p(p, k);
+    stats[4] = k;
+    stats[5] = (0.5 * p - 1.0) * log(k) - 0.5 * p * log(2.0 * CUDART_PI) - log_iv_scalar(0.5 * p - 1.0, k) + k * rbar;
+    stats[6] = A - rbar;
+    stats[7] = double(it);
+}
+
+// ---------------------------------------------------------------- scratch
+struct Scratch {
+    std::mutex mu;
+    int dev = -1;
+    void *ptr = nullptr;
+    size_t bytes = 0;
+};
+static Scratch g_scratch;
+
+static int scratch_get(size_t bytes, double **out) {
+    std::lock_guard<std::mutex> lk(g_scratch.mu);
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (g_scratch.dev != dev || g_scratch.bytes < bytes) {
+        if (g_scratch.ptr && g_scratch.dev == dev) cudaFree(g_scratch.ptr);
+        g_scratch.ptr = nullptr;
+        g_scratch.bytes = 0;
+        cudaError_t e = cudaMalloc(&g_scratch.ptr, bytes);
+        if (e != cudaSuccess) return B200_ERR_CUDA;
+        g_scratch.bytes = bytes;
+        g_scratch.dev = dev;
+    }
+    *out = static_cast<double *>(g_scratch.ptr);
+    return B200_OK;
+}
+
+static int sms_count() {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    return sms;
+}
+
+template <typename T>
+static int colsum_impl(const T *X, int64_t n, int64_t d, int64_t ld, double *colsum, int accumulate,
+                       cudaStream_t s) {
+    if (n < 0 || d < 0 || ld < d) return B200_ERR_INVALID_ARGUMENT;
+    if (d == 0) return B200_OK;
+    if (!X && n > 0) return B200_ERR_INVALID_ARGUMENT;
+    if (!colsum) return B200_ERR_INVALID_ARGUMENT;
+    if (n == 0) {
+        if (!accumulate) {
+            cudaError_t e = cudaMemsetAsync(colsum, 0, size_t(d) * sizeof(double), s);
+            return e == cudaSuccess ? B200_OK : B200_ERR_CUDA;
+        }
+        return B200_OK;
+    }
+    constexpr int VN = VecOf<T>::N;
+    const bool vec = ((reinterpret_cast<uintptr_t>(X) % 16) == 0) && ((ld * sizeof(T)) % 16 == 0);
+    const int CW = CS_TPB * (vec ? VN : 1);
+    const int64_t ncol = (d + CW - 1) / CW;
+    // ~8 CTAs per SM in total; each CTA streams a slab of rows
+    int64_t nslab = (8 * int64_t(sms_count()) + ncol - 1) / ncol;
+    if (nslab > n) nslab = n;
+    if (nslab < 1) nslab = 1;
+    const int64_t rows_per = (n + nslab - 1) / nslab;
+    nslab = (n + rows_per - 1) / rows_per;
+    double *part = nullptr;
+    int rc = scratch_get(size_t(nslab) * size_t(d) * sizeof(double), &part);
+    if (rc) return rc;
+    dim3 grid((unsigned)ncol, (unsigned)nslab);
+    if (vec)
+        colsum_partial_kernel<T, true><<<grid, CS_TPB, 0, s>>>(X, n, d, ld, rows_per, part);
+    else
+        colsum_partial_kernel<T, false><<<grid, CS_TPB, 0, s>>>(X, n, d, ld, rows_per, part);
+    const int64_t rb = (d + 255) / 256;
+    colsum_reduce_kernel<<<unsigned(rb < 4096 ? rb : 4096), 256, 0, s>>>(part, nslab, d, colsum, accumulate);
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ERR_CUDA;
+}
+
+static int fit_from_colsum_impl(const double *colsum, int64_t n_total, int64_t d, double *mu, double *stats,
+                                cudaStream_t s) {
+    if (n_total <= 0 || d < 2 || !colsum || !mu || !stats) return B200_ERR_INVALID_ARGUMENT;
+    vmf_fit_kernel<<<1, FIT_TPB, 0, s>>>(colsum, n_total, d, mu, stats);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ERR_CUDA;
+}
+
+}  // namespace b200
+
+using namespace b200;
+
+extern "C" {
+
+int b200_vmf_colsum_f32(const float *X, int64_t n, int64_t d, int64_t ld, double *colsum, int accumulate,
+                        void *stream) {
+    return colsum_impl<float>(X, n, d, ld, colsum, accumulate, static_cast<cudaStream_t>(stream));
+}
+int b200_vmf_colsum_f64(const double *X, int64_t n, int64_t d, int64_t ld, double *colsum, int accumulate,
+                        void *stream) {
+    return colsum_impl<double>(X, n, d, ld, colsum, accumulate, static_cast<cudaStream_t>(stream));
+}
+int b200_vmf_fit_from_colsum(const double *colsum, int64_t n_total, int64_t d, double *mu, double *stats,
+                             void *stream) {
+    return fit_from_colsum_impl(colsum, n_total, d, mu, stats, static_cast<cudaStream_t>(stream));
+}
+int b200_vmf_fit_f32(const float *X, int64_t n, int64_t d, double *ws, double *mu, double *stats, void *stream) {
+    int rc = colsum_impl<float>(X, n, d, d, ws, 0, static_cast<cudaStream_t>(stream));
+    if (rc) return rc;
+    return fit_from_colsum_impl(ws, n, d, mu, stats, static_cast<cudaStream_t>(stream));
+}
+int b200_vmf_fit_f64(const double *X, int64_t n, int64_t d, double *ws, double *mu, double *stats, void *stream) {
+    int rc = colsum_impl<double>(X, n, d, d, ws, 0, static_cast<cudaStream_t>(stream));
+    if (rc) return rc;
+    return fit_from_colsum_impl(ws, n, d, mu, stats, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

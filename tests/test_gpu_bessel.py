@@ -1,0 +1,229 @@
+"""GPU parity: the CUDA path (through the C ABI) against the binary128 oracle.
+
+Error measure: oracle.rel_err = |got - ref| / max(|ref|, 1)  (R1).
+Bars: 1e-13 (f64) and 1e-5 (f32) from BASELINE.json north_star; 1e-8 for the
+paper's own Simpson K fallback (its Table 2 reports 6.5e-9 in the Small region).
+"""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2409_08729_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-13
+TOL32 = 1e-5
+
+
+@pytest.fixture(scope="module")
+def B():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2409_08729_b200 as B
+    B.lib()
+    return B
+
+
+def _dev(a, dtype=torch.float64):
+    return torch.tensor(np.asarray(a), dtype=dtype, device="cuda:0")
+
+
+def _run(B, fn, v, x, dtype=torch.float64):
+    f = {"iv": B.log_iv, "kv": B.log_kv, "kvp": B.log_kv_paper}[fn]
+    out = f(_dev(v, dtype), _dev(x, dtype))
+    torch.cuda.synchronize()
+    return out.double().cpu().numpy()
+
+
+def _ref(fn, v, x):
+    return oracle.log_iv(v, x) if fn == "iv" else oracle.log_kv(v, x)
+
+
+def _check(B, fn, v, x, tol=TOL64, dtype=torch.float64, what=""):
+    got = _run(B, fn, v, x, dtype)
+    if dtype == torch.float32:   # compare at the inputs the kernel actually saw
+        v = np.asarray(v, np.float32).astype(np.float64)
+        x = np.asarray(x, np.float32).astype(np.float64)
+    ref = _ref("iv" if fn == "iv" else "kv", v, x)
+    e = oracle.rel_err(got, ref)
+    i = int(np.argmax(e)) if e.size else 0
+    assert np.all(np.isfinite(got) | np.isinf(ref)), f"{what}: non-finite output"
+    assert e.size == 0 or e[i] <= tol, f"{what} {fn}: max err {e[i]:.3e} at v={v[i]!r} x={x[i]!r} got={got[i]!r} ref={ref[i]!r}"
+    return e
+
+
+@pytest.mark.parametrize("fn", ["iv", "kv"])
+def test_config0_small_case(B, fn):
+    """BASELINE configs[0]: 10k pairs, integer v in 0..10, x ~ U[1,100]."""
+    v, x = workloads.small_case(10_000, seed=0)
+    _check(B, fn, v, x, what="configs[0]")
+
+
+@pytest.mark.parametrize("fn", ["iv", "kv"])
+@pytest.mark.parametrize("n", [0, 1, 7, 31, 1023, 1024, 1025, 4097, 65536 + 3])
+def test_ragged_sizes(B, fn, n):
+    """Tile (1024) and warp boundaries, empty input, mixed regions in one tile."""
+    rng = np.random.default_rng(n)
+    v = np.exp(rng.uniform(math.log(1e-3), math.log(2e3), n))
+    x = np.exp(rng.uniform(math.log(1e-3), math.log(2e3), n))
+    _check(B, fn, v, x, what=f"ragged n={n}")
+
+
+@pytest.mark.parametrize("fn", ["iv", "kv"])
+@pytest.mark.parametrize("region", ["small", "large"])
+def test_paper_regions(B, fn, region):
+    """PAPER.md §5.1 test regions (lines 414-416), uniform samples (§5.2)."""
+    n = 20_000 if region == "small" else 4_000
+    v, x = workloads.paper_region(n, region, fn, seed=11)
+    _check(B, fn, v, x, what=f"{region} region")
+
+
+@pytest.mark.parametrize("fn", ["iv", "kv"])
+def test_region_boundaries(B, fn):
+    """Points straddling every Table-1 threshold used on the GPU (lines 342-348)."""
+    vs, xs = [], []
+    eps = [-1e-9, 0.0, 1e-9]
+    for xt in (30.0, 59.6925, 19.6931):
+        for d in eps:
+            for v in (0.0, 0.3, 0.7, 1.0, 5.0, 12.0, 15.3919, 20.0, 100.0):
+                vs.append(v), xs.append(xt * (1 + d))
+    for vt in (15.3919, 0.7, 12.6964):
+        for d in eps:
+            for x in (1e-3, 0.5, 5.0, 19.0, 25.0, 31.0, 70.0, 1e3):
+                vs.append(vt * (1 + d)), xs.append(x)
+    lx = np.linspace(math.log(60.0), math.log(1e5), 200)
+    for l in lx:                                     # the curved mu-edge log v = 0.5113 log x + 0.7939
+        vb = math.exp(0.5113 * l + 0.7939)
+        for d in eps:
+            vs.append(vb * (1 + d)), xs.append(math.exp(l))
+    _check(B, fn, np.array(vs), np.array(xs), what="boundaries")
+
+
+@pytest.mark.parametrize("fn", ["iv", "kv"])
+def test_wide_domain(B, fn):
+    """Log-uniform over the stability domain v in [1e-3, 1e5], x in [1e-3, 1e5]."""
+    v = workloads.log_uniform(50_000, 1e-3, 1e5, seed=21)
+    x = workloads.log_uniform(50_000, 1e-3, 1e5, seed=22)
+    e = _check(B, fn, v, x, tol=5e-12, what="wide")
+    # the 1e-13 bar holds away from the eta ~ 0 band at large v
+    band = (v > 2000) & (np.abs(x / np.maximum(v, 1e-300) - 0.6627) < 0.25)
+    assert e[~band].max() <= TOL64, e[~band].max()
+
+
+@pytest.mark.parametrize("fn", ["iv", "kv"])
+def test_f32(B, fn):
+    v, x = workloads.small_case(10_000, seed=3)
+    _check(B, fn, v, x, tol=TOL32, dtype=torch.float32, what="f32 configs[0]")
+    v, x = workloads.paper_region(10_000, "small", fn, seed=4)
+    _check(B, fn, v, x, tol=TOL32, dtype=torch.float32, what="f32 small")
+
+
+def test_paper_k_integral(B):
+    """The paper's Simpson fallback: parity at the paper's own accuracy (Table 2: 6.5e-9)."""
+    v, x = workloads.paper_region(20_000, "small", "kv", seed=5)
+    got = _run(B, "kvp", v, x)
+    e = oracle.rel_err(got, oracle.log_kv(v, x))
+    assert np.all(np.isfinite(got))
+    assert e.max() <= 1e-8, e.max()
+
+
+def test_special_values(B):
+    v = np.array([0.0, 3.0, 0.0, 2.0, -1.0, 1.0, np.nan, 1.0, 20.0, 0.5])
+    x = np.array([0.0, 0.0, 1e-300, -1.0, 2.0, np.nan, 1.0, np.inf, 0.0, 1e300])
+    gi = _run(B, "iv", v, x)
+    gk = _run(B, "kv", v, x)
+    assert gi[0] == 0.0 and gi[1] == -np.inf and gi[8] == -np.inf
+    assert np.isnan(gi[3]) and np.isnan(gi[4]) and np.isnan(gi[5]) and np.isnan(gi[6])
+    assert gi[7] == np.inf
+    assert np.isfinite(gi[2])
+    assert gk[0] == np.inf and gk[1] == np.inf and gk[8] == np.inf
+    assert np.isfinite(gk[4])                      # K_{-1} = K_1
+    assert abs(gk[4] - oracle.log_kv(1.0, 2.0)) <= TOL64 * max(1, abs(gk[4]))
+    assert np.isnan(gk[3]) and np.isnan(gk[5]) and np.isnan(gk[6])
+    assert gk[7] == -np.inf
+    assert np.isfinite(gi[9]) and np.isfinite(gk[9])
+
+
+def test_negative_order_k(B):
+    v = workloads.log_uniform(5000, 1e-3, 1e3, seed=8)
+    x = workloads.log_uniform(5000, 1e-3, 1e3, seed=9)
+    a = _run(B, "kv", -v, x)
+    b = _run(B, "kv", v, x)
+    assert np.array_equal(a, b)
+
+
+def test_classify_matches_table1(B):
+    """Dispatch is Algorithm 1 / Table 1 with the GPU branch set (bit-exact ids)."""
+    rng = np.random.default_rng(12)
+    v = np.concatenate([rng.uniform(0, 200, 50_000), [1.0, 200.0, 5.0, 1.0]])
+    x = np.concatenate([rng.uniform(0, 200, 50_000), [1500.0, 10.0, 5.0, 1500.0]])
+    got = B.classify(_dev(v), _dev(x)).cpu().numpy()
+    with np.errstate(divide="ignore"):
+        mu = ((x > 30) & (v < 15.3919)) | ((0.5113 * np.log(x) + 0.7939 > np.log(v)) & (x > 59.6925))
+    u13 = ((x > 19.6931) & (v > 0.7)) | (v > 12.6964)
+    want = np.where(mu, 0, np.where(u13, 1, 2))
+    assert np.array_equal(got, want)
+    assert list(got[-4:]) == [0, 1, 2, 0]     # SPEC.md dispatch examples in batch mode
+
+
+def test_host_buffers_match_device(B):
+    v, x = workloads.bench_grid_numpy(50_000, seed=4)
+    a = B.log_iv_host(v, x)
+    b = _run(B, "iv", v, x)
+    assert np.array_equal(a, b)
+    vt = torch.tensor(v).pin_memory()
+    xt = torch.tensor(x).pin_memory()
+    c = B.log_kv_host(vt, xt).numpy()
+    d = _run(B, "kv", v, x)
+    assert np.array_equal(c, d)
+
+
+def test_deterministic(B):
+    v, x = workloads.bench_grid_numpy(20_000, seed=5)
+    assert np.array_equal(_run(B, "iv", v, x), _run(B, "iv", v, x))
+    assert np.array_equal(_run(B, "kv", v, x), _run(B, "kv", v, x))
+
+
+@pytest.mark.parametrize("fn", ["iv", "kv"])
+def test_full_bench_grid_sampled(B, fn):
+    """BASELINE configs[1]/[2] at full size (11 x 20M) in the bench launch
+    configuration; all outputs finite, 20k sampled outputs against the oracle."""
+    dev = torch.device("cuda:0")
+    v, x = workloads.bench_grid(20_000_000, seed=0, device=dev)
+    out = (B.log_iv if fn == "iv" else B.log_kv)(v, x)
+    torch.cuda.synchronize()
+    assert bool(torch.isfinite(out).all())
+    idx = torch.randint(0, v.numel(), (20_000,), generator=torch.Generator().manual_seed(1)).to(dev)
+    vs, xs, gs = v[idx].cpu().numpy(), x[idx].cpu().numpy(), out[idx].cpu().numpy()
+    e = oracle.rel_err(gs, _ref(fn, vs, xs))
+    assert e.max() <= TOL64, e.max()
+    del v, x, out
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("fn", ["iv", "kv"])
+def test_stability_sweep(B, fn):
+    """BASELINE configs[3]: v in [0,1e5] x x in [1e-3,1e5] log-spaced, 16384^2 = 268M
+    pairs: zero non-finite outputs; sampled outputs against the oracle."""
+    dev = torch.device("cuda:0")
+    total_bad = 0
+    samples_v, samples_x, samples_g = [], [], []
+    gen = torch.Generator().manual_seed(2)
+    for r0 in range(0, 16384, 4096):
+        v, x = workloads.stability_grid(16384, 16384, device=dev, rows=(r0, r0 + 4096))
+        out = (B.log_iv if fn == "iv" else B.log_kv)(v, x)
+        total_bad += int((~torch.isfinite(out)).sum().item())
+        idx = torch.randint(0, v.numel(), (1500,), generator=gen).to(dev)
+        samples_v.append(v[idx].cpu().numpy()), samples_x.append(x[idx].cpu().numpy())
+        samples_g.append(out[idx].cpu().numpy())
+        del v, x, out
+    torch.cuda.empty_cache()
+    # only x = 1e-3.. > 0 and v >= 0 in this grid: every output must be finite
+    assert total_bad == 0
+    vs, xs, gs = map(np.concatenate, (samples_v, samples_x, samples_g))
+    e = oracle.rel_err(gs, _ref(fn, vs, xs))
+    assert e.max() <= 5e-12, e.max()

@@ -1,0 +1,107 @@
+"""GPU parity of the vMF fit (§6.3) against oracle/vmf.py."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from oracle import vmf as ovmf
+from paper_2409_08729_b200 import workloads
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def B():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2409_08729_b200 as B
+    B.lib()
+    return B
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("n,d", [(1, 2), (3, 5), (1000, 64), (4097, 1030), (777, 2048)])
+def test_colsum_exact(B, dtype, n, d):
+    X, _ = workloads.vmf_features(n, d, rbar=0.4, seed=n + d, device="cuda:0", dtype=dtype)
+    got = B.vmf_colsum(X).cpu().numpy()
+    Xh = X.double().cpu().numpy()
+    ref = np.array([math.fsum(Xh[:, j]) for j in range(d)])
+    assert np.max(np.abs(got - ref)) <= 1e-13 * max(1.0, np.max(np.abs(ref))) + 1e-15 * n
+
+
+def test_colsum_strided_and_accumulate(B):
+    X, _ = workloads.vmf_features(513, 300, seed=1, device="cuda:0", dtype=torch.float32)
+    big = torch.zeros(513, 301, device="cuda:0", dtype=torch.float32)
+    big[:, :300] = X
+    view = big[:, :300]                      # ld = 301, not 16-byte aligned rows
+    a = B.vmf_colsum(view)
+    b = B.vmf_colsum(X)
+    assert torch.allclose(a, b, rtol=0, atol=1e-12)
+    c = B.vmf_colsum(X, out=b.clone(), accumulate=True)
+    assert torch.allclose(c, 2 * b, rtol=1e-15, atol=0)
+
+
+@pytest.mark.parametrize("d,rbar", [(64, 0.7), (256, 0.3), (2048, 0.15), (8192, 0.19), (2048, 0.95)])
+def test_fit_against_oracle(B, d, rbar):
+    X, _ = workloads.vmf_features(3000, d, rbar=rbar, seed=d, device="cuda:0", dtype=torch.float64)
+    mu, stats = B.vmf_fit(X)
+    s = stats.cpu().numpy()
+    ref = ovmf.fit(X.cpu().numpy())
+    assert abs(s[0] - ref["rbar"]) <= 1e-13
+    assert np.max(np.abs(mu.cpu().numpy() - ref["mu"])) <= 1e-12
+    for i, k in ((1, "kappa0"), (2, "kappa1"), (3, "kappa2")):
+        assert abs(s[i] - ref[k]) <= 1e-10 * ref[k], (k, s[i], ref[k])
+    assert abs(s[4] - ref["kappa_mle"]) <= 1e-9 * ref["kappa_mle"], (s[4], ref["kappa_mle"])
+    assert abs(s[5] - ref["loglik"]) <= 1e-10 * max(1, abs(ref["loglik"]))
+    assert abs(s[6]) <= 1e-10                                   # stationarity A_p(k) = Rbar
+    # Newton improvement ordering (Sra 2012; SPEC vmf property)
+    r = ref["rbar"]
+    g = [abs(ovmf.a_p(d, s[i]) - r) for i in (1, 2, 3)]
+    assert g[2] <= g[1] * 1.0001 + 1e-15 and g[1] <= g[0] * 1.0001 + 1e-15
+
+
+def test_table7_sufficient_statistics(B):
+    """Paper Table 7 (lines 695-711): from Rbar = A_p(kappa2_paper) the device
+    reproduces the printed kappa0/1/2 and the MLE equals kappa2 to ~1e-10."""
+    import json, os
+    rows = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "vmf_table7.json")))["rows"]
+    for r in rows:
+        p = r["p"]
+        rbar = ovmf.a_p(p, r["kappa2"])
+        colsum = torch.zeros(p, dtype=torch.float64, device="cuda:0")
+        colsum[0] = rbar * 1000.0                              # n_total = 1000, xbar = rbar e_1
+        mu, stats = B.vmf_fit_from_colsum(colsum, 1000)
+        s = stats.cpu().numpy()
+        tol = 1.5 * 10.0 ** (-r["digits"])
+        assert abs(s[1] - r["kappa0"]) <= tol and abs(s[2] - r["kappa1"]) <= tol and abs(s[3] - r["kappa2"]) <= tol
+        assert abs(s[4] - r["kappa2"]) / r["kappa2"] <= 1e-10
+
+
+def test_degenerate(B):
+    X = torch.tensor([[1.0, 0.0], [-1.0, 0.0]], dtype=torch.float64, device="cuda:0")
+    _, stats = B.vmf_fit(X)
+    s = stats.cpu().numpy()
+    assert s[0] == 0.0 and np.all(np.isnan(s[1:]))
+
+
+@pytest.mark.parametrize("d", [2048, 8192, 32768])
+def test_full_size_features(B, d):
+    """BASELINE configs[4]: 50000 x d unit-norm fp32 features (CIFAR10/ResNet50 shape)."""
+    X, _ = workloads.vmf_features(50_000, d, rbar=0.17, seed=d, device="cuda:0", dtype=torch.float32)
+    mu, stats = B.vmf_fit(X)
+    s = stats.cpu().numpy()
+    # sampled columns summed exactly on the host
+    cols = np.random.default_rng(d).choice(d, 64, replace=False)
+    Xc = X[:, torch.tensor(cols, device="cuda:0")].double().cpu().numpy()
+    colsum = B.vmf_colsum(X).cpu().numpy()
+    ref_cols = np.array([math.fsum(Xc[:, j]) for j in range(len(cols))])
+    assert np.max(np.abs(colsum[cols] - ref_cols)) <= 1e-10
+    rbar = ovmf.mean_resultant_rows(X.cpu().numpy())          # oracle input: the features only
+    assert abs(s[0] - rbar) <= 1e-12
+    k0, k1, k2 = ovmf.kappa_estimates(d, rbar)
+    km = ovmf.kappa_mle(d, rbar)
+    assert abs(s[3] - k2) <= 1e-9 * k2 and abs(s[4] - km) <= 1e-9 * km
+    del X
+    torch.cuda.empty_cache()

@@ -1,0 +1,50 @@
+"""Host logic of the CUDA path: the generated u_k(t) / 1/Gamma tables."""
+from fractions import Fraction
+
+import mpmath
+
+from paper_2409_08729_b200 import gen_tables
+
+
+def test_uk_hand_values():
+    u = gen_tables.uk_polynomials()
+    assert u[0] == {0: Fraction(1)}                                          # Eq. (u0)
+    assert u[1] == {1: Fraction(3, 24), 3: Fraction(-5, 24)}                 # (3t - 5t^3)/24
+    assert u[2] == {2: Fraction(81, 1152), 4: Fraction(-462, 1152), 6: Fraction(385, 1152)}
+    # DLMF 10.41.10: u_3 = (30375 t^3 - 369603 t^5 + 765765 t^7 - 425425 t^9)/414720
+    assert u[3] == {3: Fraction(30375, 414720), 5: Fraction(-369603, 414720),
+                    7: Fraction(765765, 414720), 9: Fraction(-425425, 414720)}
+    assert len(u) == 14 and max(u[13]) == 39 and min(u[13]) == 13
+
+
+def test_uk_recurrence_identity():
+    """u_{k+1} = (t^2 - t^4)/2 u_k' + 1/8 int_0^t (1 - 5 s^2) u_k -- checked numerically at t=0.37."""
+    mpmath.mp.dps = 40
+    u = gen_tables.uk_polynomials()
+    t = mpmath.mpf("0.37")
+    ev = lambda p, t: sum(mpmath.mpf(c.numerator) / c.denominator * t ** e for e, c in p.items())
+    for k in range(13):
+        d = mpmath.diff(lambda s: ev(u[k], s), t)
+        integ = mpmath.quad(lambda s: (1 - 5 * s * s) * ev(u[k], s), [0, t])
+        assert abs(ev(u[k + 1], t) - ((t ** 2 - t ** 4) / 2 * d + integ / 8)) < mpmath.mpf(10) ** -25
+
+
+def test_uk_t1_stirling():
+    """At t = 1, sum_k (-1)^k u_k(1)/v^k is the Stirling series of Gamma (DLMF 10.41.11 / 5.11.3):
+    u_1(1) = -1/12, u_2(1) = 1/288."""
+    u = gen_tables.uk_polynomials()
+    assert sum(u[1].values()) == Fraction(-1, 12)
+    assert sum(u[2].values()) == Fraction(1, 288)
+
+
+def test_rgamma_taylor():
+    c = gen_tables.rgamma_taylor()
+    assert c[0] == 1.0 and abs(c[1] - 0.5772156649015329) < 1e-16
+    z = 0.37
+    assert abs(sum(cj * z ** j for j, cj in enumerate(c)) - float(mpmath.rgamma(1 + z))) < 1e-16
+
+
+def test_generated_header_is_current():
+    import os
+    path = os.path.join(os.path.dirname(gen_tables.__file__), "csrc", "tables.h")
+    assert open(path).read() == gen_tables.render()
