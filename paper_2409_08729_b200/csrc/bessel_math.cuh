@@ -18,6 +18,7 @@ static __constant__ double c_uk_d[B200_UK_NCOEF] = B200_UK_TABLE_INIT;
 static __constant__ float c_uk_f[B200_UK_NCOEF] = B200_UK_TABLE_INIT;
 static __constant__ double c_rg_d[B200_RGAMMA_NT] = B200_RGAMMA_INIT;
 static __constant__ float c_rg_f[B200_RGAMMA_NT] = B200_RGAMMA_INIT;
+static __constant__ double c_eta_d[B200_ETA_NT] = B200_ETA_TAYLOR_INIT;
 
 template <typename T> struct Tr;
 template <> struct Tr<double> {
@@ -117,6 +118,28 @@ __device__ __forceinline__ T uk_row(int k, T t2) {
     return p;
 }
 
+// v * eta(x/v).  Where eta ~ 0 (z = x/v near the Laplace limit constant
+// z0 = 0.6627...) the two terms of eta cancel and plain fp64 leaves ~v*eps
+// absolute error.  There, for the f64 path, eta is evaluated
+// from its Taylor series around z0 with d = z - z0 formed from z = x/v in
+// double-double (the remainder x - z*v is exact by FMA; z - z0_hi is exact by
+// Sterbenz), so v*eta keeps full relative accuracy.
+template <typename T>
+__device__ __forceinline__ T v_times_eta(T v, T x, T z, T r) {
+    if (sizeof(T) == sizeof(double)) {
+        const double dq = double(z) - B200_ETA_Z0_HI;
+        if (fabs(dq) < 0.03) {
+            const double zlo = fma(-double(z), double(v), double(x)) / double(v);
+            const double d = dq + (zlo - B200_ETA_Z0_LO);
+            double p = c_eta_d[B200_ETA_NT - 1];
+#pragma unroll
+            for (int k = B200_ETA_NT - 2; k >= 0; --k) p = fma(p, d, c_eta_d[k]);
+            return T(double(v) * (p * d));
+        }
+    }
+    return v * (r + log(z / (T(1) + r)));
+}
+
 template <typename T, bool IS_K>
 __device__ __forceinline__ T log_bessel_u13(T v, T x) {
     const T z = x / v;
@@ -129,13 +152,13 @@ __device__ __forceinline__ T log_bessel_u13(T v, T x) {
 #pragma unroll
     for (int k = 12; k >= 1; --k) acc = fma(acc, w, uk_row<T>(k, t2));
     const T S = fabs(fma(acc, w, T(1)));
-    const T eta = r + log(z / (T(1) + r));
+    const T veta = v_times_eta<T>(v, x, z, r);
     if (!IS_K) {
         // -1/2 log(2 pi v) - 1/4 log(1+x'^2) + log|S| = log(|S| / sqrt(2 pi v r))
-        return v * eta + log(S * d_rsqrt(T(2.0 * CUDART_PI) * v * r));
+        return veta + log(S * d_rsqrt(T(2.0 * CUDART_PI) * v * r));
     } else {
         // 1/2 log(pi/(2v)) - 1/4 log(1+x'^2) + log|S| = log(|S| sqrt(pi/(2 v r)))
-        return -v * eta + log(S * d_rsqrt(T(2.0 / CUDART_PI) * v * r));
+        return -veta + log(S * d_rsqrt(T(2.0 / CUDART_PI) * v * r));
     }
 }
 

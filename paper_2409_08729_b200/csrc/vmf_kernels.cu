@@ -108,7 +108,7 @@ __device__ double newton_F(double p, double rbar, double k) {
     return k - (A - rbar) / (1.0 - A * A - (p - 1.0) / k * A);
 }
 
-constexpr int FIT_TPB = 1024;
+constexpr int FIT_TPB = 256;
 
 __global__ void __launch_bounds__(FIT_TPB) vmf_fit_kernel(const double *__restrict__ colsum, int64_t n_total,
                                                           int64_t d, double *__restrict__ mu,
