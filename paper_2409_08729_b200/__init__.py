@@ -164,14 +164,7 @@ def vmf_fit(X: torch.Tensor, process_group=None):
     row count summed, then every rank computes the same fit.
     Returns (mu, stats) with stats named by VMF_STATS.
     """
+    from .parallel import allreduce_colsum
     X = _features(X)
-    n = X.shape[0]
-    colsum = vmf_colsum(X)
-    if process_group is not None or (torch.distributed.is_available() and torch.distributed.is_initialized()
-                                     and torch.distributed.get_world_size() > 1):
-        import torch.distributed as dist
-        dist.all_reduce(colsum, group=process_group)
-        cnt = torch.tensor([float(n)], dtype=torch.float64, device=X.device)
-        dist.all_reduce(cnt, group=process_group)
-        n = int(cnt.item())
+    colsum, n = allreduce_colsum(vmf_colsum(X), X.shape[0], process_group)
     return vmf_fit_from_colsum(colsum, n)

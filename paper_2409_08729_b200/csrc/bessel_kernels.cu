@@ -27,8 +27,8 @@ namespace b200 {
 constexpr int TPB = 256;
 constexpr int ITEMS = 4;
 constexpr int TILE = TPB * ITEMS;       // 1024 pairs per tile
-constexpr int NBIN = 5;                 // 12-bit counters x 5 fit in 64 bits
-constexpr int BIN_SPECIAL = 4;
+constexpr int NBIN = 8;                 // 12-bit counters, 5 per 64-bit word, 2 words
+constexpr int BIN_SPECIAL = 7;
 
 std::atomic<int64_t> g_launches{0};
 static thread_local char g_err[256] = "";
@@ -47,8 +47,8 @@ static int cuda_err(cudaError_t e, const char *where) {
 enum : int { FN_I = 0, FN_K = 1, FN_K_PAPER = 2 };
 
 // ------------------------------------------------------------------ binning
-// bin 0 = mu, 1 = U13, 2/3 = fallback split by cost (series: x <= 8 / x > 8;
-// K: Temme series x <= 2 / Steed CF2 x > 2), 4 = special / invalid input.
+// bins 0..6 = E_MU, E_U4, E_U6, E_U9, E_U13, fallback split by cost (series:
+// x <= 8 / x > 8; K: Temme series x <= 2 / Steed CF2 x > 2); 7 = special.
 template <int FN>
 __device__ __forceinline__ int bin_of(double v, double x) {
     if (!(x > 0.0) || !isfinite(x) || !isfinite(v)) return BIN_SPECIAL;   // x<=0, NaN, inf
@@ -57,10 +57,7 @@ __device__ __forceinline__ int bin_of(double v, double x) {
     } else {
         v = fabs(v);
     }
-    const int m = select_method(v, x);
-    if (m != M_FALLBACK) return m;
-    const double split = (FN == FN_I) ? 8.0 : 2.0;
-    return x <= split ? 2 : 3;
+    return select_eval(v, x, (FN == FN_I) ? 8.0 : 2.0);
 }
 
 // Values for the special bin: x == 0, non-finite or out-of-domain inputs.
@@ -83,14 +80,35 @@ __device__ __forceinline__ T special_value(T v, T x) {
 template <typename T, int FN>
 __device__ __forceinline__ T eval_bin(int bin, T v, T x) {
     if (bin == BIN_SPECIAL) return special_value<T, FN>(v, x);
-    const int m = bin >= 2 ? M_FALLBACK : bin;
-    if (FN == FN_I) return log_iv_method<T>(m, v, x);
+    if (FN == FN_I) return log_iv_eval<T>(bin, v, x);
     const T av = fabs(v);
-    if (FN == FN_K) return log_kv_method<T, false>(m, av, x);
-    return log_kv_method<T, true>(m, av, x);
+    if (FN == FN_K) return log_kv_eval<T, false>(bin, av, x);
+    return log_kv_eval<T, true>(bin, av, x);
 }
 
-__device__ __forceinline__ int field(uint64_t packed, int b) { return int((packed >> (12 * b)) & 0xFFFull); }
+// Two 64-bit words of five 12-bit counters each (a tile has <= 1024 < 4096 of a bin).
+struct Cnt {
+    uint64_t w[2];
+    __device__ __forceinline__ void zero() { w[0] = w[1] = 0; }
+    __device__ __forceinline__ void inc(int b) {
+        const uint64_t one0 = b < 5 ? (1ull << (12 * b)) : 0ull;
+        const uint64_t one1 = b < 5 ? 0ull : (1ull << (12 * (b - 5)));
+        w[0] += one0;
+        w[1] += one1;
+    }
+    __device__ __forceinline__ int get(int b) const {
+        const uint64_t word = b < 5 ? w[0] : w[1];
+        return int((word >> (12 * (b < 5 ? b : b - 5))) & 0xFFFull);
+    }
+    __device__ __forceinline__ void add(const Cnt &o) { w[0] += o.w[0]; w[1] += o.w[1]; }
+    __device__ __forceinline__ void sub(const Cnt &o) { w[0] -= o.w[0]; w[1] -= o.w[1]; }
+    __device__ __forceinline__ Cnt shfl_up(int o) const {
+        Cnt r;
+        r.w[0] = __shfl_up_sync(0xffffffffu, w[0], o);
+        r.w[1] = __shfl_up_sync(0xffffffffu, w[1], o);
+        return r;
+    }
+};
 
 template <typename T, int FN>
 __global__ void __launch_bounds__(TPB) bessel_eval_kernel(const T *__restrict__ vin, const T *__restrict__ xin,
@@ -99,7 +117,7 @@ __global__ void __launch_bounds__(TPB) bessel_eval_kernel(const T *__restrict__ 
     __shared__ T s_x[TILE];
     __shared__ T s_res[TILE];
     __shared__ uint16_t s_idx[TILE];
-    __shared__ uint64_t s_warp[TPB / 32];
+    __shared__ Cnt s_warp[TPB / 32];
     __shared__ int s_base[NBIN + 1];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -109,7 +127,8 @@ __global__ void __launch_bounds__(TPB) bessel_eval_kernel(const T *__restrict__ 
         const int64_t base = tile * TILE;
         T lv[ITEMS], lx[ITEMS];
         int lb[ITEMS];
-        uint64_t cnt = 0;
+        Cnt cnt;
+        cnt.zero();
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
             const int64_t g = base + tid + i * TPB;
@@ -118,41 +137,44 @@ __global__ void __launch_bounds__(TPB) bessel_eval_kernel(const T *__restrict__ 
                 lv[i] = __ldg(vin + g);
                 lx[i] = __ldg(xin + g);
                 lb[i] = bin_of<FN>(double(lv[i]), double(lx[i]));
-                cnt += 1ull << (12 * lb[i]);
+                cnt.inc(lb[i]);
             }
         }
-        // block-wide exclusive scan of the packed per-thread bin counts
-        uint64_t incl = cnt;
+        // block-wide exclusive scan of the packed per-thread bin counts (warp shuffles)
+        Cnt incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint64_t y = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += y;
+            const Cnt y = incl.shfl_up(o);
+            if (lane >= o) incl.add(y);
         }
         if (lane == 31) s_warp[warp] = incl;
         __syncthreads();
         if (warp == 0) {
-            uint64_t wv = lane < TPB / 32 ? s_warp[lane] : 0ull;
-            uint64_t wi = wv;
+            Cnt wv;
+            if (lane < TPB / 32) wv = s_warp[lane]; else wv.zero();
+            Cnt wi = wv;
 #pragma unroll
             for (int o = 1; o < TPB / 32; o <<= 1) {
-                const uint64_t y = __shfl_up_sync(0xffffffffu, wi, o);
-                if (lane >= o) wi += y;
+                const Cnt y = wi.shfl_up(o);
+                if (lane >= o) wi.add(y);
             }
-            if (lane < TPB / 32) s_warp[lane] = wi - wv;     // exclusive warp offsets
+            if (lane < TPB / 32) { Cnt ex = wi; ex.sub(wv); s_warp[lane] = ex; }   // exclusive warp offsets
             if (lane == TPB / 32 - 1) {
                 int acc = 0;
-                for (int b = 0; b < NBIN; ++b) { s_base[b] = acc; acc += field(wi, b); }
+                for (int b = 0; b < NBIN; ++b) { s_base[b] = acc; acc += wi.get(b); }
                 s_base[NBIN] = acc;
             }
         }
         __syncthreads();
-        uint64_t excl = s_warp[warp] + incl - cnt;
+        Cnt excl = s_warp[warp];
+        excl.add(incl);
+        excl.sub(cnt);
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
             if (lb[i] >= 0) {
                 const int b = lb[i];
-                const int pos = s_base[b] + field(excl, b);
-                excl += 1ull << (12 * b);
+                const int pos = s_base[b] + excl.get(b);
+                excl.inc(b);
                 s_v[pos] = lv[i];
                 s_x[pos] = lx[i];
                 s_idx[pos] = uint16_t(tid + i * TPB);

@@ -19,6 +19,7 @@ static __constant__ float c_uk_f[B200_UK_NCOEF] = B200_UK_TABLE_INIT;
 static __constant__ double c_rg_d[B200_RGAMMA_NT] = B200_RGAMMA_INIT;
 static __constant__ float c_rg_f[B200_RGAMMA_NT] = B200_RGAMMA_INIT;
 static __constant__ double c_eta_d[B200_ETA_NT] = B200_ETA_TAYLOR_INIT;
+static __constant__ float c_eta_f[B200_ETA_NT] = B200_ETA_TAYLOR_INIT;
 
 template <typename T> struct Tr;
 template <> struct Tr<double> {
@@ -33,6 +34,10 @@ template <> struct Tr<float> {
     __device__ static float uk(int i) { return c_uk_f[i]; }
     __device__ static float rg(int i) { return c_rg_f[i]; }
 };
+
+// 1/k for k = 1..32 (the mu_K recurrence divides by k)
+template <typename T>
+__device__ __forceinline__ T c_inv_k(int k) { return T(1) / T(k); }
 
 // Overload helpers so templates pick the right precision.
 __device__ __forceinline__ double d_rsqrt(double a) { return rsqrt(a); }
@@ -61,28 +66,30 @@ __device__ __forceinline__ int select_method(double v, double x) {
 }
 
 // Number of terms of the mu_K expansion.  The paper uses K = 20 (Table 1);
-// we run the same recurrence to K = 26 so the truncation error stays below
-// fp64 resolution on the whole region (reading R5).
+// we allow the same recurrence up to K = 26 so the truncation error stays
+// below fp64 resolution on the whole region (reading R5), and stop
+// as soon as a term no longer changes the sum (past the initial growth of
+// the terms, k >= 4), which for x >= 60 is after 8-15 terms.
 constexpr int KMU = 26;
 
 // ---------------------------------------------------------------- mu_K
 // Eq. (log Iv mu k) (line 203-205) / Eq. (log Kv mu k) (line 234-236):
 //   log I ~ x - 1/2 log(2 pi x) + log|1 + sum_k (-1)^k prod_{j<=k}(mu-(2j-1)^2) / (k! (8x)^k)|
 //   log K ~ 1/2 (log pi - log 2x) - x + log|1 + sum_k prod_{j<=k}(mu-(2j-1)^2) / (k! (8x)^k)|
-// mu = 4 v^2.  The sum is evaluated in nested (Horner) form
-//   1 + r_1 (1 + r_2 (1 + ... r_K)),  r_k = s (mu - (2k-1)^2) / (8 x k),
-// which is the paper's term recurrence ("the terms in the series can also be
-// calculated recursively", line 208) read from the innermost term outwards.
+// mu = 4 v^2.  Terms by the paper's recurrence ("the terms in the series can
+// also be calculated recursively", line 208):
+//   term_k = term_{k-1} * s (mu - (2k-1)^2) / (8 x k),  s = -1 (I), +1 (K).
 template <typename T, bool IS_K>
 __device__ __forceinline__ T mu_series(T v, T x) {
     const T mu = T(4) * v * v;
     const T c = (IS_K ? T(1) : T(-1)) / (T(8) * x);
-    T s = T(1);
-#pragma unroll
-    for (int k = KMU; k >= 1; --k) {
+    T term = T(1), s = T(1);
+#pragma unroll 2
+    for (int k = 1; k <= KMU; ++k) {
         const T a = mu - T((2 * k - 1) * (2 * k - 1));
-        const T r = a * (c * T(1.0 / k));
-        s = fma(r, s, T(1));
+        term *= a * (c * c_inv_k<T>(k));
+        s += term;
+        if (k >= 4 && fabs(term) <= Tr<T>::eps * T(0.25) * fabs(s)) break;
     }
     return fabs(s);
 }
@@ -119,38 +126,64 @@ __device__ __forceinline__ T uk_row(int k, T t2) {
 }
 
 // v * eta(x/v).  Where eta ~ 0 (z = x/v near the Laplace limit constant
-// z0 = 0.6627...) the two terms of eta cancel and plain fp64 leaves ~v*eps
-// absolute error.  There, for the f64 path, eta is evaluated
-// from its Taylor series around z0 with d = z - z0 formed from z = x/v in
-// double-double (the remainder x - z*v is exact by FMA; z - z0_hi is exact by
+// z0 = 0.6627...) the two terms of eta cancel and plain arithmetic leaves
+// ~v*eps absolute error.  There eta is evaluated from its
+// Taylor series around z0 with d = z - z0 formed from z = x/v in two-word
+// precision (the remainder x - z*v is exact by FMA; z - z0_hi is exact by
 // Sterbenz), so v*eta keeps full relative accuracy.
+template <typename T> struct EtaC;
+template <> struct EtaC<double> {
+    static constexpr double hi = B200_ETA_Z0_HI, lo = B200_ETA_Z0_LO;
+    static constexpr int nt = B200_ETA_NT;
+    __device__ static double c(int k) { return c_eta_d[k]; }
+};
+template <> struct EtaC<float> {
+    static constexpr float hi = B200_ETA_Z0_HI_F, lo = B200_ETA_Z0_LO_F;
+    static constexpr int nt = 8;
+    __device__ static float c(int k) { return c_eta_f[k]; }
+};
+
 template <typename T>
 __device__ __forceinline__ T v_times_eta(T v, T x, T z, T r) {
-    if (sizeof(T) == sizeof(double)) {
-        const double dq = double(z) - B200_ETA_Z0_HI;
-        if (fabs(dq) < 0.03) {
-            const double zlo = fma(-double(z), double(v), double(x)) / double(v);
-            const double d = dq + (zlo - B200_ETA_Z0_LO);
-            double p = c_eta_d[B200_ETA_NT - 1];
+    const T dq = z - EtaC<T>::hi;
+    if (fabs(dq) < T(0.03)) {
+        const T zlo = fma(-z, v, x) / v;
+        const T d = dq + (zlo - EtaC<T>::lo);
+        T p = EtaC<T>::c(EtaC<T>::nt - 1);
 #pragma unroll
-            for (int k = B200_ETA_NT - 2; k >= 0; --k) p = fma(p, d, c_eta_d[k]);
-            return T(double(v) * (p * d));
-        }
+        for (int k = EtaC<T>::nt - 2; k >= 0; --k) p = fma(p, d, EtaC<T>::c(k));
+        return v * (p * d);
     }
     return v * (r + log(z / (T(1) + r)));
 }
 
-template <typename T, bool IS_K>
-__device__ __forceinline__ T log_bessel_u13(T v, T x) {
+// Number of U_K terms.  The paper's Table 1 fits regions for U4/U6/U9/U13 and
+// the GPU version keeps only U13 to avoid warp divergence (line 384).  With
+// the in-CTA binning divergence is gone, so all four come back, selected by an
+// a-priori truncation bound instead of the fitted regions (R12):
+// u_k(t) = t^k P_k(t^2) with sup_{t in [0,1]} |P_k| = P_k(0) =: M_k, and
+// w = t/v = 1/sqrt(v^2+x^2), so the first omitted term of U_K is at most
+// M_{K+1} w^{K+1} <= 2^-56 once sqrt(v^2+x^2) >= 1749 (K=4), 277 (K=6),
+// 77.6 (K=9) -- thresholds rounded up below.  U13 elsewhere (Table 1 region).
+__device__ __forceinline__ int select_u_terms(double v, double x) {
+    const double rho2 = fma(v, v, x * x);
+    if (rho2 >= 1800.0 * 1800.0) return 4;
+    if (rho2 >= 280.0 * 280.0) return 6;
+    if (rho2 >= 80.0 * 80.0) return 9;
+    return 13;
+}
+
+template <typename T, bool IS_K, int KU>
+__device__ __forceinline__ T log_bessel_u(T v, T x) {
     const T z = x / v;
     const T r2 = fma(z, z, T(1));
     const T r = sqrt(r2);
     const T t = d_rcp(r);
     const T t2 = t * t;
     const T w = (IS_K ? -t : t) / v;
-    T acc = uk_row<T>(13, t2);
+    T acc = uk_row<T>(KU, t2);
 #pragma unroll
-    for (int k = 12; k >= 1; --k) acc = fma(acc, w, uk_row<T>(k, t2));
+    for (int k = KU - 1; k >= 1; --k) acc = fma(acc, w, uk_row<T>(k, t2));
     const T S = fabs(fma(acc, w, T(1)));
     const T veta = v_times_eta<T>(v, x, z, r);
     if (!IS_K) {
@@ -344,19 +377,48 @@ __device__ __forceinline__ T log_kv_integral_paper(T v, T x) {
 }
 
 // ---------------------------------------------------------------- entry points
+// Evaluation sub-methods (bins): the region of Algorithm 1 refined by cost.
+enum : int { E_MU = 0, E_U4 = 1, E_U6 = 2, E_U9 = 3, E_U13 = 4, E_FB_A = 5, E_FB_B = 6 };
+
+__device__ __forceinline__ int select_eval(double v, double x, double fb_split) {
+    const int m = select_method(v, x);
+    if (m == M_MU) return E_MU;
+    if (m == M_U13) {
+        const int k = select_u_terms(v, x);
+        return k == 4 ? E_U4 : k == 6 ? E_U6 : k == 9 ? E_U9 : E_U13;
+    }
+    return x <= fb_split ? E_FB_A : E_FB_B;
+}
+
 template <typename T>
-__device__ __forceinline__ T log_iv_method(int m, T v, T x) {
-    if (m == M_MU) return log_iv_mu<T>(v, x);
-    if (m == M_U13) return log_bessel_u13<T, false>(v, x);
-    return log_iv_series<T>(v, x);
+__device__ __forceinline__ T log_iv_eval(int e, T v, T x) {
+    switch (e) {
+        case E_MU: return log_iv_mu<T>(v, x);
+        case E_U4: return log_bessel_u<T, false, 4>(v, x);
+        case E_U6: return log_bessel_u<T, false, 6>(v, x);
+        case E_U9: return log_bessel_u<T, false, 9>(v, x);
+        case E_U13: return log_bessel_u<T, false, 13>(v, x);
+        default: return log_iv_series<T>(v, x);
+    }
 }
 
 template <typename T, bool PAPER>
-__device__ __forceinline__ T log_kv_method(int m, T v, T x) {
-    if (m == M_MU) return log_kv_mu<T>(v, x);
-    if (m == M_U13) return log_bessel_u13<T, true>(v, x);
-    if (PAPER) return log_kv_integral_paper<T>(v, x);
-    return log_kv_fallback<T>(v, x);
+__device__ __forceinline__ T log_kv_eval(int e, T v, T x) {
+    switch (e) {
+        case E_MU: return log_kv_mu<T>(v, x);
+        case E_U4: return log_bessel_u<T, true, 4>(v, x);
+        case E_U6: return log_bessel_u<T, true, 6>(v, x);
+        case E_U9: return log_bessel_u<T, true, 9>(v, x);
+        case E_U13: return log_bessel_u<T, true, 13>(v, x);
+        default: return PAPER ? log_kv_integral_paper<T>(v, x) : log_kv_fallback<T>(v, x);
+    }
+}
+
+// Scalar entry (used by the vMF kernel): full dispatch for one element.
+template <typename T>
+__device__ __forceinline__ T log_iv_scalar_eval(T v, T x) {
+    if (x == T(0)) return v == T(0) ? T(0) : T(-CUDART_INF);
+    return log_iv_eval<T>(select_eval(double(v), double(x), 8.0), v, x);
 }
 
 }  // namespace b200

@@ -91,10 +91,7 @@ __global__ void colsum_reduce_kernel(const double *__restrict__ part, int64_t ns
 }
 
 // ---------------------------------------------------------------- scalar part
-__device__ double log_iv_scalar(double v, double x) {
-    if (x == 0.0) return v == 0.0 ? 0.0 : -CUDART_INF;
-    return log_iv_method<double>(select_method(v, x), v, x);
-}
+__device__ double log_iv_scalar(double v, double x) { return log_iv_scalar_eval<double>(v, x); }
 
 // A_p(kappa) = I_{p/2}(kappa) / I_{p/2-1}(kappa)  (line 677)
 __device__ double a_p(double p, double kappa) {

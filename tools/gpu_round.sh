@@ -24,6 +24,8 @@ for w in $WHAT; do
     launches)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
         python bench.py --steps 2 --warmup 1 --skip-e2e --skip-cpu-baseline > $OUT/launches_bench.log 2>&1 ;;
+    methods)
+      timeout 600 python tools/method_bench.py > $OUT/methods.json 2> $OUT/methods.err ;;
     full)
       timeout 1500 ncu --set full --clock-control none --import-source on -k regex:bessel_eval_kernel -s 2 -c 2 \
         -o $OUT/prof -f python bench.py --steps 1 --warmup 1 --skip-e2e --skip-cpu-baseline --n-per-v 2000000 > $OUT/ncu_full.log 2>&1 ;;
