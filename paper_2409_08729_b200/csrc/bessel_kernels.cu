@@ -111,7 +111,7 @@ struct Cnt {
 };
 
 template <typename T, int FN>
-__global__ void __launch_bounds__(TPB) bessel_eval_kernel(const T *__restrict__ vin, const T *__restrict__ xin,
+__global__ void __launch_bounds__(TPB, 3) bessel_eval_kernel(const T *__restrict__ vin, const T *__restrict__ xin,
                                                           T *__restrict__ out, int64_t n) {
     __shared__ T s_v[TILE];
     __shared__ T s_x[TILE];
@@ -123,9 +123,26 @@ __global__ void __launch_bounds__(TPB) bessel_eval_kernel(const T *__restrict__ 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t ntiles = (n + TILE - 1) / TILE;
 
+    // Software pipeline: the (v, x) of the next tile are loaded into registers
+    // while the current tile is binned and evaluated.
+    T nv[ITEMS], nx[ITEMS];
+    auto prefetch = [&](int64_t t) {
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const int64_t g = t * TILE + tid + i * TPB;
+            if (t < ntiles && g < n) {
+                nv[i] = __ldcs(vin + g);
+                nx[i] = __ldcs(xin + g);
+            }
+        }
+    };
+    prefetch(blockIdx.x);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t base = tile * TILE;
         T lv[ITEMS], lx[ITEMS];
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) { lv[i] = nv[i]; lx[i] = nx[i]; }
+        prefetch(tile + gridDim.x);
         int lb[ITEMS];
         Cnt cnt;
         cnt.zero();
@@ -134,8 +151,6 @@ __global__ void __launch_bounds__(TPB) bessel_eval_kernel(const T *__restrict__ 
             const int64_t g = base + tid + i * TPB;
             lb[i] = -1;
             if (g < n) {
-                lv[i] = __ldg(vin + g);
-                lx[i] = __ldg(xin + g);
                 lb[i] = bin_of<FN>(double(lv[i]), double(lx[i]));
                 cnt.inc(lb[i]);
             }
@@ -196,7 +211,7 @@ __global__ void __launch_bounds__(TPB) bessel_eval_kernel(const T *__restrict__ 
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
             const int64_t g = base + tid + i * TPB;
-            if (g < n) out[g] = s_res[tid + i * TPB];
+            if (g < n) __stcs(out + g, s_res[tid + i * TPB]);
         }
         __syncthreads();
     }

@@ -35,9 +35,11 @@ template <> struct Tr<float> {
     __device__ static float rg(int i) { return c_rg_f[i]; }
 };
 
-// 1/k for k = 1..32 (the mu_K recurrence divides by k)
+// 1/k for k = 1..400 (recurrences divide by the term index)
+#define B200_NINV 400
+static __constant__ double c_inv_d[B200_NINV + 1] = B200_INV_INIT;
 template <typename T>
-__device__ __forceinline__ T c_inv_k(int k) { return T(1) / T(k); }
+__device__ __forceinline__ T c_inv_k(int k) { return T(c_inv_d[k]); }
 
 // Overload helpers so templates pick the right precision.
 __device__ __forceinline__ double d_rsqrt(double a) { return rsqrt(a); }
@@ -57,9 +59,19 @@ __device__ __forceinline__ float d_rcp(float a) { return __frcp_rn(a); }
 // always taken in double so the f32 and f64 paths dispatch identically.
 enum : int { M_MU = 0, M_U13 = 1, M_FALLBACK = 2 };
 
+// The curved mu edge [0.5113 log x + 0.7939 > log v] is decided with the
+// hardware log2 (MUFU.LG2, fp32) and re-evaluated in double only inside a
+// 1e-4 guard band, so the result equals the double-precision predicate.
+__device__ __forceinline__ bool mu_edge(double v, double x) {
+    const float lx = __log2f(float(x)), lv = __log2f(float(v));
+    const float d = 0.5113f * lx + 1.14535832f - lv;   // 0.7939 / ln 2 = 1.14535832
+    if (fabsf(d) > 1e-4f) return d > 0.0f;
+    return 0.5113 * log(x) + 0.7939 > log(v);
+}
+
 __device__ __forceinline__ int select_method(double v, double x) {
     bool mu = (x > 30.0) && (v < 15.3919);
-    if (!mu && x > 59.6925) mu = (0.5113 * log(x) + 0.7939 > log(v));
+    if (!mu && x > 59.6925) mu = (v <= 0.0) || mu_edge(v, x);
     if (mu) return M_MU;
     if ((x > 19.6931 && v > 0.7) || v > 12.6964) return M_U13;
     return M_FALLBACK;
@@ -212,11 +224,15 @@ __device__ __forceinline__ T log_iv_series(T v, T x) {
     if (x == T(0)) return v == T(0) ? T(0) : T(-CUDART_INF);
     const T q = T(0.25) * x * x;
     T b = T(1), S = T(1);
-    for (int k = 0; k < 200; ++k) {
-        const T d = (T(k) + T(1)) * (T(k) + v + T(1));
-        b = b * q / d;
-        S += b;
-        if (d > q && b <= S * Tr<T>::eps) break;
+    // b_{k+1} = b_k * q * (1/(k+1)) * (1/(k+v+1)): 1/(k+1) from the table, the
+    // reciprocal of (k+v+1) does not depend on b, so it is off the dependency chain.
+    for (int k = 0; k < 200; k += 2) {
+        const T r0 = q * c_inv_k<T>(k + 1) / (T(k) + v + T(1));
+        const T r1 = q * c_inv_k<T>(k + 2) / (T(k) + v + T(2));
+        const T b0 = b * r0;
+        b = b0 * r1;
+        S += b0 + b;
+        if (r1 < T(1) && b <= S * Tr<T>::eps) break;
     }
     return v * log(T(0.5) * x) - d_lgamma(v + T(1)) + log(S);
 }
@@ -272,10 +288,12 @@ __device__ __forceinline__ T temme_kmu(T mu, T x, T &rho) {
         const T m2 = mu * mu;
         for (int i = 1; i < 100; ++i) {
             const T fi = T(i);
-            ff = (fi * ff + p + q) / (fi * fi - m2);
-            c *= dd / fi;
-            p /= (fi - mu);
-            q /= (fi + mu);
+            // 1/(i-mu), 1/(i+mu) and 1/(i^2-mu^2) share one reciprocal
+            const T inv = T(1) / (fi * fi - m2);
+            ff = (fi * ff + p + q) * inv;
+            c *= dd * c_inv_k<T>(i);
+            p *= (fi + mu) * inv;
+            q *= (fi - mu) * inv;
             const T del = c * ff;
             sum += del;
             sum1 += c * (p - fi * ff);
@@ -293,10 +311,9 @@ __device__ __forceinline__ T temme_kmu(T mu, T x, T &rho) {
         T q = a1, c = a1;
         T a = -a1;
         T s = T(1) + q * delh;
-        for (int i = 1; i < 400; ++i) {
-            const T fi = T(i);
+        for (int i = 1; i < B200_NINV; ++i) {
             a -= T(2 * i);
-            c = -a * c / (fi + T(1));
+            c = -a * c * c_inv_k<T>(i + 1);
             const T qnew = (q1 - b * q2) / a;
             q1 = q2;
             q2 = qnew;

@@ -52,20 +52,28 @@ def test_fit_against_oracle(B, d, rbar):
     assert abs(s[0] - ref["rbar"]) <= 1e-13
     assert np.max(np.abs(mu.cpu().numpy() - ref["mu"])) <= 1e-12
     assert abs(s[1] - ref["kappa0"]) <= 1e-12 * ref["kappa0"]
-    # kappa1 = F(kappa0), kappa2 = F(kappa1): a Newton step divides by
-    # A'(k) = 1 - A^2 - (p-1)/k A, which cancels as Rbar -> 1, so an error
-    # delta in A_p moves the step by |step| (2A + (p-1)/k) delta / |A'|.
-    # delta is bounded by the log I parity bar: 1e-13 * max(|log I|, 1) (x2 logs).
+    # kappa1 = F(kappa0), kappa2 = F(kappa1), kappa_mle = A_p^{-1}(Rbar).  All
+    # divide by A'(k) = 1 - A^2 - (p-1)/k A, which cancels as Rbar -> 1
+    # (A' ~ (p-1)/(2k^2)).  An error delta in A_p (relative) moves F by
+    # [A + |step| (2A + (p-1)/k)] A delta / |A'|.  delta = difference of two
+    # log I values, each computed with O(1) roundings of size eps |log I|:
+    # delta = 2 * 32 eps max(|log I|, 1).
+    eps = 2.0 ** -53
+
+    def cond_tol(k_at, step, kref):
+        A = ovmf.a_p(d, k_at)
+        dA = abs(1 - A * A - (d - 1) / k_at * A)
+        delta = 64 * eps * max(abs(float(oracle.log_iv(d / 2, k_at))), 1.0)
+        return 1e-12 * kref + (A + abs(step) * (2 * A + (d - 1) / k_at)) * A * delta / dA
+
     prev = ref["kappa0"]
     for i, k in ((2, "kappa1"), (3, "kappa2")):
-        A = ovmf.a_p(d, prev)
-        dA = 1 - A * A - (d - 1) / prev * A
-        lI = abs(float(oracle.log_iv(d / 2, prev)))
-        delta = 2e-13 * max(lI, 1.0)
-        tol = 1e-12 * ref[k] + abs(ref[k] - prev) * (2 * A + (d - 1) / prev) * delta / abs(dA)
+        tol = cond_tol(prev, ref[k] - prev, ref[k])
         assert abs(s[i] - ref[k]) <= tol, (k, s[i], ref[k], tol)
         prev = ref[k]
-    assert abs(s[4] - ref["kappa_mle"]) <= 1e-9 * ref["kappa_mle"], (s[4], ref["kappa_mle"])
+    km = ref["kappa_mle"]
+    tol = max(1e-9 * km, cond_tol(km, 0.0, km))
+    assert abs(s[4] - km) <= tol, (s[4], km, tol)
     assert abs(s[5] - ref["loglik"]) <= 1e-10 * max(1, abs(ref["loglik"]))
     assert abs(s[6]) <= 1e-10                                   # stationarity A_p(k) = Rbar
     # Newton improvement ordering (Sra 2012; SPEC vmf property)
