@@ -34,10 +34,15 @@ UNIT = "Gevals/s"
 N_PER_V = 20_000_000
 N_ORDERS = 11
 BYTES_PER_EVAL = 24          # read v, x (2 x 8 B), write out (8 B)  -- DESIGN.md §Roofline
-# FP64 operations per evaluation of the dominant kernel, from the ncu
-# instruction counts of the bench workload (profiles/).
-# None until measured: roofline then reports the HBM bound only.
-FP64_FLOP_PER_EVAL = {"log_iv": None, "log_kv": None}
+# FP64 operations (DADD + DMUL + 2*DFMA, thread level) and DRAM bytes per
+# evaluation of the dominant kernel, from the ncu --set full capture of the
+# bench workload promoted to profiles/roofline_counts.json
+# (tools/summarize_profiles.py --promote).
+
+
+def _roofline_counts():
+    p = os.path.join(ROOT, "profiles", "roofline_counts.json")
+    return json.load(open(p)) if os.path.exists(p) else {}
 
 
 def _env_int(name, default):
@@ -274,14 +279,20 @@ def run_ours(args):
             "traffic": None, "kernel": f"bessel_eval_kernel ({dom})", "peak_source": hbm_src,
             "kernel_ms": dom_ms}
     fp64_peak, fp64_src = _fp64_peak()
-    fl = FP64_FLOP_PER_EVAL.get(dom)
+    cnt = _roofline_counts().get(dom, {})
+    fl = cnt.get("fp64_flop_per_eval")
+    if cnt.get("dram_bytes_per_eval"):
+        roof["traffic"] = cnt["dram_bytes_per_eval"] * n
+        roof["traffic_source"] = cnt["source"] + ", scaled per evaluation to this launch"
     if fl and fp64_peak:
         tf = fl * n / (dom_ms / 1e3) / 1e12
         if tf / fp64_peak > gbs / hbm_peak:
             roof = {"bound": "alu", "achieved": tf, "peak": fp64_peak, "unit": "TFLOP/s",
-                    "frac": tf / fp64_peak, "traffic": None, "kernel": f"bessel_eval_kernel ({dom})",
-                    "peak_source": fp64_src, "kernel_ms": dom_ms, "fp64_flop_per_eval": fl,
-                    "hbm_frac": gbs / hbm_peak}
+                    "frac": tf / fp64_peak, "traffic": roof.get("traffic"),
+                    "kernel": f"bessel_eval_kernel ({dom})", "peak_source": fp64_src,
+                    "kernel_ms": dom_ms, "fp64_flop_per_eval": fl, "flop_source": cnt["source"],
+                    "hbm": {"achieved_gbs": gbs, "peak_gbs": hbm_peak, "frac": gbs / hbm_peak,
+                            "algorithmic_bytes_per_eval": BYTES_PER_EVAL}}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
