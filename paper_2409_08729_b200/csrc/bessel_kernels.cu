@@ -24,8 +24,18 @@
 
 namespace b200 {
 
-constexpr int TPB = 256;
-constexpr int ITEMS = 4;
+// Launch shape (overridable only by tools/variant_bench.py experiments).
+#ifndef B200_TPB
+#define B200_TPB 256
+#endif
+#ifndef B200_MINB
+#define B200_MINB 3
+#endif
+#ifndef B200_ITEMS
+#define B200_ITEMS 4
+#endif
+constexpr int TPB = B200_TPB;
+constexpr int ITEMS = B200_ITEMS;
 constexpr int TILE = TPB * ITEMS;       // 1024 pairs per tile
 constexpr int NBIN = 8;                 // 12-bit counters, 5 per 64-bit word, 2 words
 constexpr int BIN_SPECIAL = 7;
@@ -80,6 +90,9 @@ __device__ __forceinline__ T special_value(T v, T x) {
 template <typename T, int FN>
 __device__ __forceinline__ T eval_bin(int bin, T v, T x) {
     if (bin == BIN_SPECIAL) return special_value<T, FN>(v, x);
+#ifdef B200_EVAL_NOP
+    return v + x;   // experiment only: measures the tile machinery alone
+#endif
     if (FN == FN_I) return log_iv_eval<T>(bin, v, x);
     const T av = fabs(v);
     if (FN == FN_K) return log_kv_eval<T, false>(bin, av, x);
@@ -111,7 +124,7 @@ struct Cnt {
 };
 
 template <typename T, int FN>
-__global__ void __launch_bounds__(TPB, 3) bessel_eval_kernel(const T *__restrict__ vin, const T *__restrict__ xin,
+__global__ void __launch_bounds__(TPB, B200_MINB) bessel_eval_kernel(const T *__restrict__ vin, const T *__restrict__ xin,
                                                           T *__restrict__ out, int64_t n) {
     __shared__ T s_v[TILE];
     __shared__ T s_x[TILE];
