@@ -37,6 +37,7 @@ namespace b200 {
 constexpr int TPB = B200_TPB;
 constexpr int ITEMS = B200_ITEMS;
 constexpr int TILE = TPB * ITEMS;       // 1024 pairs per tile
+static_assert(TILE <= 4096, "s_idx packs a 12-bit tile index with the bin");
 constexpr int NBIN = 8;                 // 12-bit counters, 5 per 64-bit word, 2 words
 constexpr int BIN_SPECIAL = 7;
 
@@ -205,7 +206,7 @@ __global__ void __launch_bounds__(TPB, B200_MINB) bessel_eval_kernel(const T *__
                 excl.inc(b);
                 s_v[pos] = lv[i];
                 s_x[pos] = lx[i];
-                s_idx[pos] = uint16_t(tid + i * TPB);
+                s_idx[pos] = uint16_t((tid + i * TPB) | (b << 12));   // tile index | bin
             }
         }
         __syncthreads();
@@ -214,10 +215,8 @@ __global__ void __launch_bounds__(TPB, B200_MINB) bessel_eval_kernel(const T *__
         for (int i = 0; i < ITEMS; ++i) {
             const int p = tid + i * TPB;
             if (p < total) {
-                int bin = 0;
-#pragma unroll
-                for (int b = 1; b < NBIN; ++b) bin += (p >= s_base[b]);
-                s_res[s_idx[p]] = eval_bin<T, FN>(bin, s_v[p], s_x[p]);
+                const int w = s_idx[p];
+                s_res[w & 0xFFF] = eval_bin<T, FN>(w >> 12, s_v[p], s_x[p]);
             }
         }
         __syncthreads();

@@ -9,6 +9,7 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include "fastmath.cuh"
 #include "tables.h"
 
 namespace b200 {
@@ -42,22 +43,24 @@ template <typename T>
 __device__ __forceinline__ T c_inv_k(int k) { return T(c_inv_d[k]); }
 
 // Overload helpers so templates pick the right precision.
-__device__ __forceinline__ double d_rsqrt(double a) { return rsqrt(a); }
-__device__ __forceinline__ float d_rsqrt(float a) { return rsqrtf(a); }
 __device__ __forceinline__ double d_sinpi(double a) { return sinpi(a); }
 __device__ __forceinline__ float d_sinpi(float a) { return sinpif(a); }
 __device__ __forceinline__ double d_lgamma(double a) { return lgamma(a); }
 __device__ __forceinline__ float d_lgamma(float a) { return lgammaf(a); }
-__device__ __forceinline__ double d_rcp(double a) { return 1.0 / a; }
-__device__ __forceinline__ float d_rcp(float a) { return __frcp_rn(a); }
 
 // ---------------------------------------------------------------- dispatch
 // Algorithm 1 / Table 1 (lines 338-352), with the
 // GPU branch set: "When running on a GPU the branches for the mu_3, U_4, U_6,
 // U_9 expressions are removed" (line 384).  Predicates read as strict
-// inequalities with natural logarithms (reading R3).  Logs are
-// always taken in double so the f32 and f64 paths dispatch identically.
+// inequalities with natural logarithms (reading R3), decided in
+// double on both precisions (the f32 and f64 paths dispatch identically).
+// For non-negative doubles the IEEE bit pattern orders like the value, so
+// each "x > C" is one 64-bit integer compare (ALU pipe) instead of a DSETP
+// on the FP64 pipe -- the same predicate, bit for bit.
 enum : int { M_MU = 0, M_U13 = 1, M_FALLBACK = 2 };
+
+__device__ __forceinline__ long long dbits(double a) { return __double_as_longlong(a); }
+#define B200_GT(a_bits, C) ((a_bits) > dbits(C))
 
 // The curved mu edge [0.5113 log x + 0.7939 > log v] is decided with the
 // hardware log2 (MUFU.LG2, fp32) and re-evaluated in double only inside a
@@ -69,11 +72,13 @@ __device__ __forceinline__ bool mu_edge(double v, double x) {
     return 0.5113 * log(x) + 0.7939 > log(v);
 }
 
+// v >= 0, x > 0 (callers filter the rest)
 __device__ __forceinline__ int select_method(double v, double x) {
-    bool mu = (x > 30.0) && (v < 15.3919);
-    if (!mu && x > 59.6925) mu = (v <= 0.0) || mu_edge(v, x);
+    const long long bv = dbits(v), bx = dbits(x);
+    bool mu = B200_GT(bx, 30.0) && bv < dbits(15.3919);           // x > 30 && v < 15.3919
+    if (!mu && B200_GT(bx, 59.6925)) mu = (bv <= 0) || mu_edge(v, x);   // v <= 0 || edge
     if (mu) return M_MU;
-    if ((x > 19.6931 && v > 0.7) || v > 12.6964) return M_U13;
+    if ((B200_GT(bx, 19.6931) && B200_GT(bv, 0.7)) || B200_GT(bv, 12.6964)) return M_U13;
     return M_FALLBACK;
 }
 
@@ -84,40 +89,48 @@ __device__ __forceinline__ int select_method(double v, double x) {
 // the terms, k >= 4), which for x >= 60 is after 8-15 terms.
 constexpr int KMU = 26;
 
+// Wide-range guard: the fast paths form 1/x, v^2 + x^2 and 1/rho, which stay
+// normal for arguments below BIG; beyond it the same formulas run rescaled or
+// through the CUDA library functions (never on the tested domain).
+template <typename T> struct Big;
+template <> struct Big<double> { static constexpr double v = 1e150; };
+template <> struct Big<float> { static constexpr float v = 1e18f; };
+
 // ---------------------------------------------------------------- mu_K
 // Eq. (log Iv mu k) (line 203-205) / Eq. (log Kv mu k) (line 234-236):
 //   log I ~ x - 1/2 log(2 pi x) + log|1 + sum_k (-1)^k prod_{j<=k}(mu-(2j-1)^2) / (k! (8x)^k)|
 //   log K ~ 1/2 (log pi - log 2x) - x + log|1 + sum_k prod_{j<=k}(mu-(2j-1)^2) / (k! (8x)^k)|
 // mu = 4 v^2.  Terms by the paper's recurrence ("the terms in the series can
 // also be calculated recursively", line 208):
-//   term_k = term_{k-1} * s (mu - (2k-1)^2) / (8 x k),  s = -1 (I), +1 (K).
+//   term_k = term_{k-1} * s (mu - (2k-1)^2) / (8 x k),  s = -1 (I), +1 (K),
+// fully unrolled so (2k-1)^2 and 1/k are compile-time constants; the stop
+// test runs every second term.
 template <typename T, bool IS_K>
-__device__ __forceinline__ T mu_series(T v, T x) {
+__device__ __forceinline__ T mu_series(T v, T rx) {
     const T mu = T(4) * v * v;
-    const T c = (IS_K ? T(1) : T(-1)) / (T(8) * x);
+    const T c = (IS_K ? T(0.125) : T(-0.125)) * rx;
     T term = T(1), s = T(1);
-#pragma unroll 2
+#pragma unroll
     for (int k = 1; k <= KMU; ++k) {
-        const T a = mu - T((2 * k - 1) * (2 * k - 1));
-        term *= a * (c * c_inv_k<T>(k));
+        term *= (mu - T((2 * k - 1) * (2 * k - 1))) * (c * T(1.0 / k));
         s += term;
-        if (k >= 4 && fabs(term) <= Tr<T>::eps * T(0.25) * fabs(s)) break;
+        if ((k & 1) == 0 && k >= 4 && fabs(term) <= Tr<T>::eps * T(0.25) * fabs(s)) break;
     }
     return fabs(s);
 }
 
-template <typename T>
-__device__ __forceinline__ T log_iv_mu(T v, T x) {
-    // x - 1/2 log(2 pi x) + log|S|  =  x + log(|S| / sqrt(2 pi x))
-    const T S = mu_series<T, false>(v, x);
-    return x + log(S * d_rsqrt(T(2.0 * CUDART_PI) * x));
-}
-
-template <typename T>
-__device__ __forceinline__ T log_kv_mu(T v, T x) {
-    // 1/2 (log pi - log 2x) - x + log|S|  =  -x + log(|S| sqrt(pi / 2x))
-    const T S = mu_series<T, true>(v, x);
-    return -x + log(S * d_rsqrt(T(2.0 / CUDART_PI) * x));
+// log I = x - 1/2 log(2 pi x) + log S = x + 1/2 log(S^2 / (2 pi x))  (one log)
+template <typename T, bool IS_K>
+__device__ __forceinline__ T log_bessel_mu(T v, T x) {
+    if (x < Big<T>::v) {
+        const T rx = fm_rcp(x);
+        const T S = mu_series<T, IS_K>(v, rx);
+        const T c = IS_K ? T(CUDART_PI / 2.0) : T(0.5 / CUDART_PI);
+        return (IS_K ? -x : x) + T(0.5) * fm_log(S * S * rx * c);
+    }
+    const T S = mu_series<T, IS_K>(v, T(1) / x);
+    const T l2 = IS_K ? T(-0.22579135264472743) : T(1.8378770664093453);   // log(2/pi), log(2 pi)
+    return (IS_K ? -x : x) + log(S) - T(0.5) * (l2 + log(x));
 }
 
 // ---------------------------------------------------------------- U_13
@@ -127,6 +140,13 @@ __device__ __forceinline__ T log_kv_mu(T v, T x) {
 //   log K ~  1/2 log(pi/(2v)) - v eta - 1/4 log(1+x'^2) + log|1 + sum_k (-1)^k u_k(t)/v^k|
 // u_k(t) = t^k P_k(t^2) (tables.h, generated from Eqs. (u0),(uk)).  With
 // w = +-t/v the sum is w (P_1 + w (P_2 + ... + w P_13)).
+//
+// Evaluated through rho = sqrt(v^2 + x^2) = v sqrt(1+x'^2), one reciprocal
+// square root y = 1/rho giving all of
+//   t = v y,   t/v = y,   v sqrt(1+x'^2) = rho,   x'/(1+sqrt(1+x'^2)) = x/(v+rho),
+//   -1/2 log(2 pi v) - 1/4 log(1+x'^2) = 1/2 log(y / (2 pi)),
+// so log I = rho + v log(x/(v+rho)) + 1/2 log(S^2 y / (2 pi)): two logs, no
+// division, no sqrt (the algebra is exact; only rounding differs).
 template <typename T>
 __device__ __forceinline__ T uk_row(int k, T t2) {
     // P_k(t2) by Horner, k+1 coefficients starting at UK_OFF[k]
@@ -155,18 +175,21 @@ template <> struct EtaC<float> {
     __device__ static float c(int k) { return c_eta_f[k]; }
 };
 
+// vs, xs, rhos: v, x, rho scaled by the same power of two s; returns v*eta.
 template <typename T>
-__device__ __forceinline__ T v_times_eta(T v, T x, T z, T r) {
-    const T dq = z - EtaC<T>::hi;
-    if (fabs(dq) < T(0.03)) {
-        const T zlo = fma(-z, v, x) / v;
-        const T d = dq + (zlo - EtaC<T>::lo);
+__device__ __forceinline__ T v_times_eta(T v, T x, T vs, T xs, T rhos, T rho) {
+    // band test on z = x/v without a division: |x - z0 v| < 0.03 v
+    if (fabs(fma(-EtaC<T>::hi, v, x)) < T(0.03) * v) {
+        const T rv = T(1) / v;
+        const T z = x * rv;
+        const T zlo = fma(-z, v, x) * rv;
+        const T d = (z - EtaC<T>::hi) + (zlo - EtaC<T>::lo);
         T p = EtaC<T>::c(EtaC<T>::nt - 1);
 #pragma unroll
         for (int k = EtaC<T>::nt - 2; k >= 0; --k) p = fma(p, d, EtaC<T>::c(k));
         return v * (p * d);
     }
-    return v * (r + log(z / (T(1) + r)));
+    return fma(v, fm_log_wide(xs * fm_rcp(vs + rhos)), rho);
 }
 
 // Number of U_K terms.  The paper's Table 1 fits regions for U4/U6/U9/U13 and
@@ -176,35 +199,40 @@ __device__ __forceinline__ T v_times_eta(T v, T x, T z, T r) {
 // u_k(t) = t^k P_k(t^2) with sup_{t in [0,1]} |P_k| = P_k(0) =: M_k, and
 // w = t/v = 1/sqrt(v^2+x^2), so the first omitted term of U_K is at most
 // M_{K+1} w^{K+1} <= 2^-56 once sqrt(v^2+x^2) >= 1749 (K=4), 277 (K=6),
-// 77.6 (K=9) -- thresholds rounded up below.  U13 elsewhere (Table 1 region).
+// 77.6 (K=9) -- thresholds rounded up below (with room for the fp32 rounding
+// of rho^2, which is formed in single precision here: an upper bound test).
 __device__ __forceinline__ int select_u_terms(double v, double x) {
-    const double rho2 = fma(v, v, x * x);
-    if (rho2 >= 1800.0 * 1800.0) return 4;
-    if (rho2 >= 280.0 * 280.0) return 6;
-    if (rho2 >= 80.0 * 80.0) return 9;
+    const float vf = float(v), xf = float(x);
+    const float rho2 = fmaf(vf, vf, xf * xf);
+    if (rho2 >= 1800.0f * 1800.0f) return 4;
+    if (rho2 >= 280.0f * 280.0f) return 6;
+    if (rho2 >= 80.0f * 80.0f) return 9;
     return 13;
 }
 
 template <typename T, bool IS_K, int KU>
 __device__ __forceinline__ T log_bessel_u(T v, T x) {
-    const T z = x / v;
-    const T r2 = fma(z, z, T(1));
-    const T r = sqrt(r2);
-    const T t = d_rcp(r);
+    // rescale by a power of two where v^2 + x^2 could overflow (wide-range guard)
+    const bool big = fmax(v, x) >= Big<T>::v;
+    const T s = big ? T(1.0 / 1267650600228229401496703205376.0) : T(1);     // 2^-100
+    const T ls = big ? T(-69.31471805599453) : T(0);                         // log s
+    const T vs = v * s, xs = x * s;
+    const T rho2 = fma(vs, vs, xs * xs);
+    const T y = fm_rsqrt(rho2);                  // 1 / (s rho)
+    const T rhos = rho2 * y;
+    const T rho = big ? rhos * T(1267650600228229401496703205376.0) : rhos;
+    const T t = vs * y;
     const T t2 = t * t;
-    const T w = (IS_K ? -t : t) / v;
+    const T w = (IS_K ? -y : y) * s;             // +-t/v
     T acc = uk_row<T>(KU, t2);
 #pragma unroll
     for (int k = KU - 1; k >= 1; --k) acc = fma(acc, w, uk_row<T>(k, t2));
     const T S = fabs(fma(acc, w, T(1)));
-    const T veta = v_times_eta<T>(v, x, z, r);
-    if (!IS_K) {
-        // -1/2 log(2 pi v) - 1/4 log(1+x'^2) + log|S| = log(|S| / sqrt(2 pi v r))
-        return veta + log(S * d_rsqrt(T(2.0 * CUDART_PI) * v * r));
-    } else {
-        // 1/2 log(pi/(2v)) - 1/4 log(1+x'^2) + log|S| = log(|S| sqrt(pi/(2 v r)))
-        return -veta + log(S * d_rsqrt(T(2.0 / CUDART_PI) * v * r));
-    }
+    const T veta = v_times_eta<T>(v, x, vs, xs, rhos, rho);
+    // 1/2 log(S^2 y_true c) with y_true = s y
+    const T c = IS_K ? T(CUDART_PI / 2.0) : T(0.5 / CUDART_PI);
+    const T tail = T(0.5) * (fm_log(S * S * y * c) + ls);
+    return IS_K ? tail - veta : veta + tail;
 }
 
 // ---------------------------------------------------------------- series (I)
@@ -232,15 +260,21 @@ __device__ __forceinline__ T log_iv_series(T v, T x) {
     if constexpr (sizeof(T) == 8) {
         const T q = T(0.25) * x * x;
         T N = T(1), P = T(1), Q = T(1), vk = v;
-        for (int k = 1; k < 400; ++k) {
+        for (int k = 1; k < 400; k += 2) {
             vk += T(1);
-            const T d = T(k) * vk;
+            const T d0 = T(k) * vk;
             Q *= q;
-            N = fma(N, d, Q);
-            P *= d;
+            N = fma(N, d0, Q);
+            P *= d0;
+            vk += T(1);
+            const T d1 = T(k + 1) * vk;
+            Q *= q;
+            N = fma(N, d1, Q);
+            P *= d1;
             if (Q <= N * Tr<T>::eps) break;
         }
-        return v * log(T(0.5) * x) - d_lgamma(v + T(1)) + log(N / P);
+        const T lx = (x >= T(1e-300)) ? fm_log(T(0.5) * x) : log(T(0.5) * x);
+        return fma(v, lx, fm_log(fm_div(N, P)) - d_lgamma(v + T(1)));
     }
     const T q = T(0.25) * x * x;
     T b = T(1), S = T(1);
@@ -261,12 +295,12 @@ __device__ __forceinline__ T log_iv_series(T v, T x) {
 // Small-argument region of K (x <= 30, v <= 12.7 after dispatch).  The paper
 // evaluates Eq. (log Kv integral) with Simpson N = 600 (lines 248-324); its
 // measured error against the binary128 oracle is up to 5.7e-10 (DESIGN.md
-// §K-fallback), above the 1e-13 target.  We use Temme's method instead:
-// K_mu, K_{mu+1} for |mu| <= 1/2 by Temme's series (x <= 2) or Steed's
-// continued fraction CF2 (x > 2), then the forward recurrence
-// K_{nu+1} = K_{nu-1} + (2 nu / x) K_nu (stable for K) up to nu = v, with the
-// running value kept as mantissa * 2^e so nothing overflows; the result is
-// returned as a logarithm.
+// §5), above the 1e-13 target.  Instead, for x <= 2 Temme's method:
+// K_mu, K_{mu+1} for |mu| <= 1/2 by Temme's series, then the forward
+// recurrence K_{nu+1} = K_{nu-1} + (2 nu / x) K_nu (stable for K) up to
+// nu = v, with the running value kept as mantissa * 10^(30 e) so nothing
+// overflows; the result is returned as a logarithm.  For 2 < x <= 30 the
+// trapezoidal rule on DLMF 10.32.9 (log_kv_trapezoid below).
 template <typename T>
 __device__ __forceinline__ void temme_gammas(T mu, T &gam1, T &gam2, T &gampl, T &gammi) {
     // 1/Gamma(1+z) = sum_j c_j z^j  (tables.h).  Even/odd parts give
@@ -286,11 +320,11 @@ __device__ __forceinline__ void temme_gammas(T mu, T &gam1, T &gam2, T &gampl, T
     gammi = ev - mu * od;   // 1/Gamma(1-mu)
 }
 
-// returns log K_mu(x) and rho = K_{mu+1}(x) / K_mu(x)
+// returns log K_mu(x) and rho = K_{mu+1}(x) / K_mu(x), for 0 < x <= 2 (Temme's series)
 template <typename T>
 __device__ __forceinline__ T temme_kmu(T mu, T x, T &rho) {
     const T eps = Tr<T>::eps;
-    if (x <= T(2)) {
+    {
         const T d = -log(T(0.5) * x);       // ln(2/x)
         const T e = mu * d;
         const T fact = (mu == T(0)) ? T(1) : (T(CUDART_PI) * mu) / d_sinpi(mu);
@@ -321,35 +355,6 @@ __device__ __forceinline__ T temme_kmu(T mu, T x, T &rho) {
         }
         rho = (T(2) / x) * (sum1 / sum);
         return log(sum);
-    } else {
-        const T m2 = mu * mu;
-        T b = T(2) * (T(1) + x);
-        T d = T(1) / b;
-        T h = d, delh = d;
-        T q1 = T(0), q2 = T(1);
-        const T a1 = T(0.25) - m2;
-        T q = a1, c = a1;
-        T a = -a1;
-        T s = T(1) + q * delh;
-        for (int i = 1; i < B200_NINV; ++i) {
-            a -= T(2 * i);
-            c = -a * c * c_inv_k<T>(i + 1);
-            const T qnew = (q1 - b * q2) / a;
-            q1 = q2;
-            q2 = qnew;
-            q += c * qnew;
-            b += T(2);
-            d = T(1) / (b + a * d);
-            delh = (b * d - T(1)) * delh;
-            h += delh;
-            const T dels = q * delh;
-            s += dels;
-            if (fabs(dels) < fabs(s) * eps) break;
-        }
-        h = a1 * h;
-        rho = (mu + x + T(0.5) - h) / x;
-        // K_mu = sqrt(pi/(2x)) e^{-x} / s
-        return -x - log(s * d_rsqrt(T(CUDART_PI / 2.0) / x));
     }
 }
 
@@ -366,18 +371,18 @@ __device__ __forceinline__ T temme_kmu(T mu, T x, T &rho) {
 static __constant__ double c_ktrap_d[B200_KTRAP_N] = B200_KTRAP_INIT;
 template <typename T>
 __device__ __forceinline__ T log_kv_trapezoid(T v, T x) {
-    const T E = exp(v * T(B200_KTRAP_H));
-    const T Ei = T(1) / E;
+    const T E = fm_exp(v * T(B200_KTRAP_H));
+    const T Ei = fm_rcp(E);
     T ek = T(1), eik = T(1), S = T(1), prev = T(CUDART_INF);
     for (int k = 1; k < B200_KTRAP_N; ++k) {
         ek *= E;
         eik *= Ei;
-        const T term = exp(-x * T(c_ktrap_d[k])) * (ek + eik);
+        const T term = fm_exp(-x * T(c_ktrap_d[k])) * (ek + eik);
         S += term;
         if (term <= S * Tr<T>::eps && term <= prev) break;
         prev = term;
     }
-    return -x + log(T(0.5 * B200_KTRAP_H) * S);
+    return -x + fm_log(T(0.5 * B200_KTRAP_H) * S);
 }
 
 template <typename T>
@@ -458,7 +463,7 @@ __device__ __forceinline__ int select_eval(double v, double x, double fb_split) 
 template <typename T>
 __device__ __forceinline__ T log_iv_eval(int e, T v, T x) {
     switch (e) {
-        case E_MU: return log_iv_mu<T>(v, x);
+        case E_MU: return log_bessel_mu<T, false>(v, x);
         case E_U4: return log_bessel_u<T, false, 4>(v, x);
         case E_U6: return log_bessel_u<T, false, 6>(v, x);
         case E_U9: return log_bessel_u<T, false, 9>(v, x);
@@ -470,7 +475,7 @@ __device__ __forceinline__ T log_iv_eval(int e, T v, T x) {
 template <typename T, bool PAPER>
 __device__ __forceinline__ T log_kv_eval(int e, T v, T x) {
     switch (e) {
-        case E_MU: return log_kv_mu<T>(v, x);
+        case E_MU: return log_bessel_mu<T, true>(v, x);
         case E_U4: return log_bessel_u<T, true, 4>(v, x);
         case E_U6: return log_bessel_u<T, true, 6>(v, x);
         case E_U9: return log_bessel_u<T, true, 9>(v, x);

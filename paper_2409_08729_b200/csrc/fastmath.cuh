@@ -1,0 +1,115 @@
+// fastmath.cuh -- f64 elementary functions for the evaluation kernels.
+//
+// CUDA's libdevice log/exp/sqrt/division handle every IEEE corner case
+// (denormals, infinities, NaN, overflow) with range checks and slow-path
+// branches; on sm_100a a double log() costs ~80 instructions, of which only
+// ~20 issue on the FP64 pipe (ncu, profiles/r02).  The dispatch of Algorithm 1
+// only ever hands these functions finite, normal, in-range arguments, so the
+// kernels use the table-driven versions below instead:
+//   fm_log : 256-entry table of 1/c_i and -log(1/c_i) (hi+lo), |r| < 2^-9,
+//            degree-6 Taylor polynomial of log1p(r);  error < 1 ulp + 2^-60 abs.
+//   fm_exp : 2^(j/64) table (hi+lo), |r| < ln2/128, degree-5 expm1 polynomial.
+//   fm_rcp / fm_rsqrt : MUFU seed (rcp/rsqrt.approx.ftz.f64), a cubic and a Newton step.
+// Argument contracts are stated per function; callers guarantee them.  The
+// float overloads forward to the CUDA single-precision functions (the f32 path
+// is not on the bench).  Tables: tables.h (paper_2409_08729_b200/gen_tables.py).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "tables.h"
+
+namespace b200 {
+
+struct LogEnt { double invc, thi, tlo, pad; };
+static __device__ const LogEnt g_logtab[1 << B200_LOG_TAB_BITS] = B200_LOGTAB_INIT_STRUCT;
+static __device__ const double2 g_exptab[B200_EXP_TAB_N] = B200_EXPTAB_INIT_STRUCT;
+
+// ln 2 split so that e * LN2_HI is exact for |e| < 2^11 (fdlibm constants)
+constexpr double LN2_HI = 6.93147180369123816490e-01;
+constexpr double LN2_LO = 1.90821492927058770002e-10;
+
+// log(a) for finite normal a > 0.
+__device__ __forceinline__ double fm_log(double a) {
+    const int hi = __double2hiint(a), lo = __double2loint(a);
+    const int t = hi - B200_LOG_HI_OFF;
+    const int e = t >> 20;                                   // a = 2^e * m, m in [sqrt(1/2), sqrt(2))
+    const int i = (t >> (20 - B200_LOG_TAB_BITS)) & ((1 << B200_LOG_TAB_BITS) - 1);
+    const double m = __hiloint2double(hi - (e << 20), lo);
+    const double2 c = __ldg(reinterpret_cast<const double2 *>(&g_logtab[i]));
+    const double tlo = __ldg(&g_logtab[i].tlo);
+    const double r = fma(m, c.x, -1.0);                      // m / c_i - 1, |r| < 0.00195
+    // log1p(r) - r = r^2 (-1/2 + r (1/3 + r (-1/4 + r (1/5 - r/6))))
+    double p = fma(r, -1.0 / 6.0, 0.2);
+    p = fma(p, r, -0.25);
+    p = fma(p, r, 1.0 / 3.0);
+    p = fma(p, r, -0.5);
+    const double ed = double(e);
+    const double h = fma(ed, LN2_HI, c.y);
+    const double l = fma(ed, LN2_LO, tlo);
+    return h + (r + fma(r * r, p, l));
+}
+
+// exp(y) for -708 <= y <= 709 (result normal); y < -708 is clamped (callers
+// only use it where such terms are negligible).
+__device__ __forceinline__ double fm_exp(double y) {
+    constexpr double SHIFT = 6755399441055744.0;               // 1.5 * 2^52: round-to-int
+    constexpr double INV = 92.33248261689366;                 // 64 / ln 2
+    constexpr double C_HI = 0.010830424695086549;              // ln2/64, 33 significant bits
+    constexpr double C_LO = 1.162596423439437e-12;             // ln2/64 - C_HI
+    y = fmax(y, -708.0);
+    double kd = fma(y, INV, SHIFT);
+    const int k = __double2loint(kd);
+    kd -= SHIFT;
+    double r = fma(kd, -C_HI, y);
+    r = fma(kd, -C_LO, r);                                     // |r| <= ln2/128
+    // expm1(r) = r + r^2 (1/2 + r (1/6 + r (1/24 + r/120)))
+    double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
+    p = fma(p, r, 1.0 / 6.0);
+    p = fma(p, r, 0.5);
+    p = fma(p, r * r, r);
+    const double2 T = __ldg(&g_exptab[k & (B200_EXP_TAB_N - 1)]);
+    const double res = T.x + fma(T.x, p, T.y);
+    return __hiloint2double(__double2hiint(res) + ((k >> 6) << 20), __double2loint(res));
+}
+
+// 1/a for finite normal |a| in [2^-1000, 2^1000].
+__device__ __forceinline__ double fm_rcp(double a) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+    double e = fma(-a, r, 1.0);
+    r = fma(r, fma(e, e, e), r);              // cubic step: error e^3
+    e = fma(-a, r, 1.0);
+    return fma(r, e, r);                      // Newton step
+}
+
+// x / y (y as for fm_rcp), with one residual correction (faithful).
+__device__ __forceinline__ double fm_div(double x, double y) {
+    const double r = fm_rcp(y);
+    const double q = x * r;
+    return fma(r, fma(-y, q, x), q);
+}
+
+// 1/sqrt(a) for finite normal a > 0 in [2^-1000, 2^1000].
+__device__ __forceinline__ double fm_rsqrt(double a) {
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+    double e = fma(-a * y, y, 1.0);           // 1 - a y^2
+    y = fma(y, e * fma(e, 0.375, 0.5), y);    // y (1 + e/2 + 3e^2/8): error O(e^3)
+    e = fma(-a * y, y, 1.0);
+    return fma(0.5 * y, e, y);                // Newton step
+}
+
+// log(a) for any finite a > 0 (subnormals through the library function).
+__device__ __forceinline__ double fm_log_wide(double a) { return a >= 1e-300 ? fm_log(a) : log(a); }
+
+// f32 path: the CUDA single-precision functions.
+__device__ __forceinline__ float fm_log_wide(float a) { return logf(a); }
+__device__ __forceinline__ float fm_log(float a) { return logf(a); }
+__device__ __forceinline__ float fm_exp(float y) { return expf(y); }
+__device__ __forceinline__ float fm_rcp(float a) { return __frcp_rn(a); }
+__device__ __forceinline__ float fm_div(float x, float y) { return x / y; }
+__device__ __forceinline__ float fm_rsqrt(float a) { return rsqrtf(a); }
+
+}  // namespace b200

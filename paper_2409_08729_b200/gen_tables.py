@@ -97,6 +97,49 @@ def ktrap_nodes(h: float = KTRAP_H, n: int = KTRAP_N):
     return [float(2 * mpmath.sinh(mpmath.mpf(k) * mpmath.mpf(h) / 2) ** 2) for k in range(n)]
 
 
+# Table-driven f64 log/exp of csrc/fastmath.cuh.
+LOG_TAB_BITS = 8
+LOG_HI_OFF = 0x3FE6A09E      # high word of sqrt(1/2): mantissas are reduced to [sqrt(1/2), sqrt(2))
+EXP_TAB_N = 64
+
+
+def log_table():
+    """Entry i covers the high words [OFF + i*2^12, OFF + (i+1)*2^12) of a number in
+    [sqrt(1/2), sqrt(2)); invc_i = 1/(bucket centre) rounded to double and
+    -log(invc_i) split into hi + lo (mpmath, 60 digits).  The bucket holding 1.0
+    gets invc = 1 exactly so log(1 + r) keeps full relative accuracy near 1."""
+    import struct
+
+    import mpmath
+    mpmath.mp.dps = 60
+
+    def hw2d(h):
+        return struct.unpack("<d", struct.pack("<Q", (h & 0xFFFFFFFF) << 32))[0]
+    rows = []
+    one_bucket = (0x3FF00000 - LOG_HI_OFF) >> (20 - LOG_TAB_BITS)
+    for i in range(1 << LOG_TAB_BITS):
+        lo = hw2d(LOG_HI_OFF + (i << (20 - LOG_TAB_BITS)))
+        hi = hw2d(LOG_HI_OFF + ((i + 1) << (20 - LOG_TAB_BITS)))
+        invc = 1.0 if i == one_bucket else float(2 / (mpmath.mpf(lo) + mpmath.mpf(hi)))
+        t = -mpmath.log(mpmath.mpf(invc))
+        th = float(t)
+        tl = float(t - mpmath.mpf(th))
+        rows.append((invc, th, tl))
+    return rows
+
+
+def exp_table(n: int = EXP_TAB_N):
+    """2^(j/n), j = 0..n-1, as hi + lo (mpmath, 60 digits)."""
+    import mpmath
+    mpmath.mp.dps = 60
+    out = []
+    for j in range(n):
+        t = mpmath.power(2, mpmath.mpf(j) / n)
+        h = float(t)
+        out.append((h, float(t - mpmath.mpf(h))))
+    return out
+
+
 def render() -> str:
     lines = [
         "// GENERATED by paper_2409_08729_b200/gen_tables.py -- do not edit.",
@@ -130,6 +173,15 @@ def render() -> str:
     lines.append("#define B200_KTRAP_H %r" % KTRAP_H)
     lines.append("#define B200_KTRAP_N %d" % KTRAP_N)
     lines.append("#define B200_KTRAP_INIT { %s }" % ", ".join("%.17e" % c for c in ktrap_nodes()))
+    lines.append("")
+    lines.append("// f64 log table (csrc/fastmath.cuh): {1/c_i, -log(1/c_i) hi, lo, 0}, i = 0..%d" % ((1 << LOG_TAB_BITS) - 1))
+    lines.append("#define B200_LOG_TAB_BITS %d" % LOG_TAB_BITS)
+    lines.append("#define B200_LOG_HI_OFF 0x%08X" % LOG_HI_OFF)
+    lines.append("#define B200_LOGTAB_INIT_STRUCT { %s }" % ", ".join(
+        "{%.17e, %.17e, %.17e, 0.0}" % r for r in log_table()))
+    lines.append("// f64 exp table: 2^(j/%d) hi, lo" % EXP_TAB_N)
+    lines.append("#define B200_EXP_TAB_N %d" % EXP_TAB_N)
+    lines.append("#define B200_EXPTAB_INIT_STRUCT { %s }" % ", ".join("{%.17e, %.17e}" % r for r in exp_table()))
     lines.append("")
     hi, lo, ce = eta_root_taylor()
     lines.append("// eta(z) = sqrt(1+z^2) + log(z/(1+sqrt(1+z^2))): root z0 = HI + LO and")
