@@ -29,7 +29,7 @@ namespace b200 {
 #define B200_TPB 256
 #endif
 #ifndef B200_MINB
-#define B200_MINB 3
+#define B200_MINB 4
 #endif
 #ifndef B200_ITEMS
 #define B200_ITEMS 4
@@ -38,7 +38,7 @@ constexpr int TPB = B200_TPB;
 constexpr int ITEMS = B200_ITEMS;
 constexpr int TILE = TPB * ITEMS;       // 1024 pairs per tile
 static_assert(TILE <= 4096, "s_idx packs a 12-bit tile index with the bin");
-constexpr int NBIN = 8;                 // 12-bit counters, 5 per 64-bit word, 2 words
+constexpr int NBIN = 8;
 constexpr int BIN_SPECIAL = 7;
 
 std::atomic<int64_t> g_launches{0};
@@ -59,21 +59,22 @@ enum : int { FN_I = 0, FN_K = 1, FN_K_PAPER = 2 };
 
 // ------------------------------------------------------------------ binning
 // bins 0..6 = E_MU, E_U4, E_U6, E_U9, E_U13, fallback split by cost (series:
-// x <= 8 / x > 8; K: Temme series x <= 2 / Steed CF2 x > 2); 7 = special.
+// x <= 8 / x > 8; K: Temme series x <= 2 / trapezoid x > 2); 7 = special.
+// The domain tests run on the IEEE bit patterns (integer pipe): x must lie in
+// (0, +inf), v must be finite, and for I v >= 0 (-0.0 counts as 0).
 template <int FN>
 __device__ __forceinline__ int bin_of(double v, double x) {
-    if (!(x > 0.0) || !isfinite(x) || !isfinite(v)) return BIN_SPECIAL;   // x<=0, NaN, inf
-    if (FN == FN_I) {
-        if (v < 0.0) return BIN_SPECIAL;
-    } else {
-        v = fabs(v);
-    }
-    return select_eval(v, x, (FN == FN_I) ? 8.0 : 2.0);
+    const long long bx = dbits(x), bv = dbits(v);
+    const long long av = bv & 0x7FFFFFFFFFFFFFFFll;                         // |v|
+    if ((unsigned long long)(bx - 1) >= 0x7FEFFFFFFFFFFFFFull) return BIN_SPECIAL;   // x <= 0, inf, NaN
+    if (av >= 0x7FF0000000000000ll) return BIN_SPECIAL;                    // v inf / NaN
+    if (FN == FN_I && bv < 0 && av != 0) return BIN_SPECIAL;               // v < 0
+    return select_eval_bits(__longlong_as_double(av), x, av, bx, (FN == FN_I) ? 8.0 : 2.0);
 }
 
 // Values for the special bin: x == 0, non-finite or out-of-domain inputs.
 template <typename T, int FN>
-__device__ __forceinline__ T special_value(T v, T x) {
+__device__ __noinline__ T special_value(T v, T x) {
     const T nan = T(CUDART_NAN);
     if (isnan(v) || isnan(x) || x < T(0)) return nan;
     if (FN == FN_I) {
@@ -100,29 +101,22 @@ __device__ __forceinline__ T eval_bin(int bin, T v, T x) {
     return log_kv_eval<T, true>(bin, av, x);
 }
 
-// Two 64-bit words of five 12-bit counters each (a tile has <= 1024 < 4096 of a bin).
-struct Cnt {
-    uint64_t w[2];
-    __device__ __forceinline__ void zero() { w[0] = w[1] = 0; }
-    __device__ __forceinline__ void inc(int b) {
-        const uint64_t one0 = b < 5 ? (1ull << (12 * b)) : 0ull;
-        const uint64_t one1 = b < 5 ? 0ull : (1ull << (12 * (b - 5)));
-        w[0] += one0;
-        w[1] += one1;
-    }
-    __device__ __forceinline__ int get(int b) const {
-        const uint64_t word = b < 5 ? w[0] : w[1];
-        return int((word >> (12 * (b < 5 ? b : b - 5))) & 0xFFFull);
-    }
-    __device__ __forceinline__ void add(const Cnt &o) { w[0] += o.w[0]; w[1] += o.w[1]; }
-    __device__ __forceinline__ void sub(const Cnt &o) { w[0] -= o.w[0]; w[1] -= o.w[1]; }
-    __device__ __forceinline__ Cnt shfl_up(int o) const {
-        Cnt r;
-        r.w[0] = __shfl_up_sync(0xffffffffu, w[0], o);
-        r.w[1] = __shfl_up_sync(0xffffffffu, w[1], o);
-        return r;
-    }
-};
+// Counting-sort helpers.  A thread bins ITEMS <= 8 elements, so per-thread and
+// warp-inclusive counts (<= 32 * ITEMS <= 255) fit 8-bit fields: all 8 bins in
+// one 64-bit word, scanned across the warp with 64-bit shuffles.  Across warps
+// (counts up to TILE) the fields are widened to 16 bits, bins 0-3 / 4-7.
+__device__ __forceinline__ uint64_t widen_lo(uint64_t c8) {   // bytes 0..3 -> 16-bit fields
+    const uint32_t a = uint32_t(c8);
+    return uint64_t(__byte_perm(a, 0, 0x4140)) | (uint64_t(__byte_perm(a, 0, 0x4342)) << 32);
+}
+__device__ __forceinline__ uint64_t widen_hi(uint64_t c8) {   // bytes 4..7 -> 16-bit fields
+    const uint32_t a = uint32_t(c8 >> 32);
+    return uint64_t(__byte_perm(a, 0, 0x4140)) | (uint64_t(__byte_perm(a, 0, 0x4342)) << 32);
+}
+__device__ __forceinline__ uint64_t shfl_up64(uint64_t v, int o) { return __shfl_up_sync(0xffffffffu, v, o); }
+__device__ __forceinline__ uint64_t shfl64(uint64_t v, int l) { return __shfl_sync(0xffffffffu, v, l); }
+
+static_assert(ITEMS <= 7, "8-bit warp-level bin counters hold at most 255 = 32 * 7 + 31");
 
 template <typename T, int FN>
 __global__ void __launch_bounds__(TPB, B200_MINB) bessel_eval_kernel(const T *__restrict__ vin, const T *__restrict__ xin,
@@ -131,8 +125,8 @@ __global__ void __launch_bounds__(TPB, B200_MINB) bessel_eval_kernel(const T *__
     __shared__ T s_x[TILE];
     __shared__ T s_res[TILE];
     __shared__ uint16_t s_idx[TILE];
-    __shared__ Cnt s_warp[TPB / 32];
-    __shared__ int s_base[NBIN + 1];
+    __shared__ uint64_t s_wtot[TPB / 32];          // per-warp bin totals, 8-bit fields
+    __shared__ ulonglong2 s_off[TPB / 32];         // per-warp bin offsets, 16-bit fields
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t ntiles = (n + TILE - 1) / TILE;
@@ -141,91 +135,100 @@ __global__ void __launch_bounds__(TPB, B200_MINB) bessel_eval_kernel(const T *__
     // while the current tile is binned and evaluated.
     T nv[ITEMS], nx[ITEMS];
     auto prefetch = [&](int64_t t) {
+        if (t >= ntiles) return;
+        const int64_t base = t * TILE;
+        const int rem = int(n - base < TILE ? n - base : TILE);
+        const T *pv = vin + base + tid, *px = xin + base + tid;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-            const int64_t g = t * TILE + tid + i * TPB;
-            if (t < ntiles && g < n) {
-                nv[i] = __ldcs(vin + g);
-                nx[i] = __ldcs(xin + g);
+            if (tid + i * TPB < rem) {
+                nv[i] = __ldcs(pv + i * TPB);
+                nx[i] = __ldcs(px + i * TPB);
             }
         }
     };
     prefetch(blockIdx.x);
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t base = tile * TILE;
+        const int rem = int(n - base < TILE ? n - base : TILE);
         T lv[ITEMS], lx[ITEMS];
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) { lv[i] = nv[i]; lx[i] = nx[i]; }
         prefetch(tile + gridDim.x);
         int lb[ITEMS];
-        Cnt cnt;
-        cnt.zero();
+        uint64_t c8 = 0;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-            const int64_t g = base + tid + i * TPB;
             lb[i] = -1;
-            if (g < n) {
+            if (tid + i * TPB < rem) {
                 lb[i] = bin_of<FN>(double(lv[i]), double(lx[i]));
-                cnt.inc(lb[i]);
+                c8 += 1ull << (8 * lb[i]);
             }
         }
-        // block-wide exclusive scan of the packed per-thread bin counts (warp shuffles)
-        Cnt incl = cnt;
+        // warp-inclusive scan of the packed counts
+        uint64_t incl = c8;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const Cnt y = incl.shfl_up(o);
-            if (lane >= o) incl.add(y);
+            const uint64_t y = shfl_up64(incl, o);
+            if (lane >= o) incl += y;
         }
-        if (lane == 31) s_warp[warp] = incl;
+        if (lane == 31) s_wtot[warp] = incl;
         __syncthreads();
         if (warp == 0) {
-            Cnt wv;
-            if (lane < TPB / 32) wv = s_warp[lane]; else wv.zero();
-            Cnt wi = wv;
+            // lanes 0..NW-1: exclusive scan over warps of the per-bin totals (16-bit
+            // fields), plus the bin bases from the tile totals (lane NW-1)
+            constexpr int NW = TPB / 32;
+            const uint64_t t8 = lane < NW ? s_wtot[lane] : 0ull;
+            const uint64_t lo = widen_lo(t8), hi = widen_hi(t8);
+            uint64_t ilo = lo, ihi = hi;
 #pragma unroll
-            for (int o = 1; o < TPB / 32; o <<= 1) {
-                const Cnt y = wi.shfl_up(o);
-                if (lane >= o) wi.add(y);
+            for (int o = 1; o < NW; o <<= 1) {
+                const uint64_t ylo = shfl_up64(ilo, o), yhi = shfl_up64(ihi, o);
+                if (lane >= o) { ilo += ylo; ihi += yhi; }
             }
-            if (lane < TPB / 32) { Cnt ex = wi; ex.sub(wv); s_warp[lane] = ex; }   // exclusive warp offsets
-            if (lane == TPB / 32 - 1) {
-                int acc = 0;
-                for (int b = 0; b < NBIN; ++b) { s_base[b] = acc; acc += wi.get(b); }
-                s_base[NBIN] = acc;
-            }
+            const uint64_t tlo = shfl64(ilo, NW - 1), thi = shfl64(ihi, NW - 1);   // tile totals per bin
+            // exclusive prefix over bins: field k of (x * 0x0001000100010001) is sum_{j<=k}
+            constexpr uint64_t ONES = 0x0001000100010001ull;
+            const uint64_t plo = tlo * ONES;
+            const uint64_t blo = plo - tlo;                                        // bases of bins 0..3
+            const uint64_t bhi = thi * ONES - thi + (plo >> 48) * ONES;            // bases of bins 4..7
+            if (lane < NW) s_off[lane] = make_ulonglong2(blo + ilo - lo, bhi + ihi - hi);
         }
         __syncthreads();
-        Cnt excl = s_warp[warp];
-        excl.add(incl);
-        excl.sub(cnt);
+        // this thread's first slot per bin: warp offset + warp-exclusive count
+        const ulonglong2 wo = s_off[warp];
+        const uint64_t ex8 = incl - c8;
+        uint64_t plo = wo.x + widen_lo(ex8), phi = wo.y + widen_hi(ex8);
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-            if (lb[i] >= 0) {
-                const int b = lb[i];
-                const int pos = s_base[b] + excl.get(b);
-                excl.inc(b);
+            const int b = lb[i];
+            if (b >= 0) {
+                const int sh = 16 * (b & 3);
+                const uint64_t word = b < 4 ? plo : phi;
+                const int pos = int((word >> sh) & 0xFFFFull);
+                if (b < 4) plo += 1ull << sh; else phi += 1ull << sh;
                 s_v[pos] = lv[i];
                 s_x[pos] = lx[i];
                 s_idx[pos] = uint16_t((tid + i * TPB) | (b << 12));   // tile index | bin
             }
         }
         __syncthreads();
-        const int total = s_base[NBIN];
 #pragma unroll 1
         for (int i = 0; i < ITEMS; ++i) {
             const int p = tid + i * TPB;
-            if (p < total) {
+            if (p < rem) {
                 const int w = s_idx[p];
                 s_res[w & 0xFFF] = eval_bin<T, FN>(w >> 12, s_v[p], s_x[p]);
             }
         }
         __syncthreads();
+        // (no trailing barrier: the next tile writes shared memory only after its
+        // first barrier, which every thread reaches after this store)
+        T *po = out + base + tid;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-            const int64_t g = base + tid + i * TPB;
-            if (g < n) __stcs(out + g, s_res[tid + i * TPB]);
+            if (tid + i * TPB < rem) __stcs(po + i * TPB, s_res[tid + i * TPB]);
         }
-        __syncthreads();
     }
 }
 

@@ -72,14 +72,17 @@ __device__ __forceinline__ bool mu_edge(double v, double x) {
     return 0.5113 * log(x) + 0.7939 > log(v);
 }
 
-// v >= 0, x > 0 (callers filter the rest)
-__device__ __forceinline__ int select_method(double v, double x) {
-    const long long bv = dbits(v), bx = dbits(x);
+// v >= 0, x > 0 (callers filter the rest); bv, bx = dbits(v), dbits(x)
+__device__ __forceinline__ int select_method_bits(double v, double x, long long bv, long long bx) {
     bool mu = B200_GT(bx, 30.0) && bv < dbits(15.3919);           // x > 30 && v < 15.3919
     if (!mu && B200_GT(bx, 59.6925)) mu = (bv <= 0) || mu_edge(v, x);   // v <= 0 || edge
     if (mu) return M_MU;
     if ((B200_GT(bx, 19.6931) && B200_GT(bv, 0.7)) || B200_GT(bv, 12.6964)) return M_U13;
     return M_FALLBACK;
+}
+
+__device__ __forceinline__ int select_method(double v, double x) {
+    return select_method_bits(v, x, dbits(v), dbits(x));
 }
 
 // Number of terms of the mu_K expansion.  The paper uses K = 20 (Table 1);
@@ -112,7 +115,9 @@ __device__ __forceinline__ T mu_series(T v, T rx) {
     T term = T(1), s = T(1);
 #pragma unroll
     for (int k = 1; k <= KMU; ++k) {
-        term *= (mu - T((2 * k - 1) * (2 * k - 1))) * (c * T(1.0 / k));
+        T inv_k;
+        if constexpr (sizeof(T) == 8) inv_k = c_inv_d[k]; else inv_k = T(1.0 / k);
+        term *= (mu - T((2 * k - 1) * (2 * k - 1))) * (c * inv_k);
         s += term;
         if ((k & 1) == 0 && k >= 4 && fabs(term) <= Tr<T>::eps * T(0.25) * fabs(s)) break;
     }
@@ -450,14 +455,17 @@ __device__ __forceinline__ T log_kv_integral_paper(T v, T x) {
 // Evaluation sub-methods (bins): the region of Algorithm 1 refined by cost.
 enum : int { E_MU = 0, E_U4 = 1, E_U6 = 2, E_U9 = 3, E_U13 = 4, E_FB_A = 5, E_FB_B = 6 };
 
-__device__ __forceinline__ int select_eval(double v, double x, double fb_split) {
-    const int m = select_method(v, x);
+__device__ __forceinline__ int select_eval_bits(double v, double x, long long bv, long long bx, double fb_split) {
+    const int m = select_method_bits(v, x, bv, bx);
     if (m == M_MU) return E_MU;
     if (m == M_U13) {
         const int k = select_u_terms(v, x);
         return k == 4 ? E_U4 : k == 6 ? E_U6 : k == 9 ? E_U9 : E_U13;
     }
-    return x <= fb_split ? E_FB_A : E_FB_B;
+    return B200_GT(bx, fb_split) ? E_FB_B : E_FB_A;
+}
+__device__ __forceinline__ int select_eval(double v, double x, double fb_split) {
+    return select_eval_bits(v, x, dbits(v), dbits(x), fb_split);
 }
 
 template <typename T>

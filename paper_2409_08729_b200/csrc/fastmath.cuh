@@ -26,9 +26,21 @@ struct LogEnt { double invc, thi, tlo, pad; };
 static __device__ const LogEnt g_logtab[1 << B200_LOG_TAB_BITS] = B200_LOGTAB_INIT_STRUCT;
 static __device__ const double2 g_exptab[B200_EXP_TAB_N] = B200_EXPTAB_INIT_STRUCT;
 
-// ln 2 split so that e * LN2_HI is exact for |e| < 2^11 (fdlibm constants)
-constexpr double LN2_HI = 6.93147180369123816490e-01;
-constexpr double LN2_LO = 1.90821492927058770002e-10;
+// Polynomial and reduction constants.  Kept in constant memory rather than as
+// literals: a double literal whose low word is non-zero costs two UMOVs per
+// use in SASS, a __constant__ operand is fetched two at a time (LDCU.128).
+struct FmConst {
+    double log_c6, log_c5, log_c3;       // -1/6, 1/5, 1/3
+    double ln2_hi, ln2_lo;               // ln 2 split so that e * ln2_hi is exact for |e| < 2^11 (fdlibm)
+    double exp_inv, exp_chi, exp_clo;    // 64/ln2; ln2/64 = chi (33 significant bits) + clo
+    double exp_c5, exp_c4, exp_c3;       // 1/120, 1/24, 1/6
+};
+static __constant__ FmConst c_fm = {
+    -1.0 / 6.0, 0.2, 1.0 / 3.0,
+    6.93147180369123816490e-01, 1.90821492927058770002e-10,
+    92.33248261689366, 0.010830424695086549, 1.162596423439437e-12,
+    1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0,
+};
 
 // log(a) for finite normal a > 0.
 __device__ __forceinline__ double fm_log(double a) {
@@ -41,32 +53,29 @@ __device__ __forceinline__ double fm_log(double a) {
     const double tlo = __ldg(&g_logtab[i].tlo);
     const double r = fma(m, c.x, -1.0);                      // m / c_i - 1, |r| < 0.00195
     // log1p(r) - r = r^2 (-1/2 + r (1/3 + r (-1/4 + r (1/5 - r/6))))
-    double p = fma(r, -1.0 / 6.0, 0.2);
+    double p = fma(r, c_fm.log_c6, c_fm.log_c5);
     p = fma(p, r, -0.25);
-    p = fma(p, r, 1.0 / 3.0);
+    p = fma(p, r, c_fm.log_c3);
     p = fma(p, r, -0.5);
     const double ed = double(e);
-    const double h = fma(ed, LN2_HI, c.y);
-    const double l = fma(ed, LN2_LO, tlo);
+    const double h = fma(ed, c_fm.ln2_hi, c.y);
+    const double l = fma(ed, c_fm.ln2_lo, tlo);
     return h + (r + fma(r * r, p, l));
 }
 
 // exp(y) for -708 <= y <= 709 (result normal); y < -708 is clamped (callers
 // only use it where such terms are negligible).
 __device__ __forceinline__ double fm_exp(double y) {
-    constexpr double SHIFT = 6755399441055744.0;               // 1.5 * 2^52: round-to-int
-    constexpr double INV = 92.33248261689366;                 // 64 / ln 2
-    constexpr double C_HI = 0.010830424695086549;              // ln2/64, 33 significant bits
-    constexpr double C_LO = 1.162596423439437e-12;             // ln2/64 - C_HI
+    constexpr double SHIFT = 6755399441055744.0;               // 1.5 * 2^52: round-to-int (immediate)
     y = fmax(y, -708.0);
-    double kd = fma(y, INV, SHIFT);
+    double kd = fma(y, c_fm.exp_inv, SHIFT);
     const int k = __double2loint(kd);
     kd -= SHIFT;
-    double r = fma(kd, -C_HI, y);
-    r = fma(kd, -C_LO, r);                                     // |r| <= ln2/128
+    double r = fma(kd, -c_fm.exp_chi, y);
+    r = fma(kd, -c_fm.exp_clo, r);                             // |r| <= ln2/128
     // expm1(r) = r + r^2 (1/2 + r (1/6 + r (1/24 + r/120)))
-    double p = fma(r, 1.0 / 120.0, 1.0 / 24.0);
-    p = fma(p, r, 1.0 / 6.0);
+    double p = fma(r, c_fm.exp_c5, c_fm.exp_c4);
+    p = fma(p, r, c_fm.exp_c3);
     p = fma(p, r, 0.5);
     p = fma(p, r * r, r);
     const double2 T = __ldg(&g_exptab[k & (B200_EXP_TAB_N - 1)]);
