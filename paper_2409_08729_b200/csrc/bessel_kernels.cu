@@ -38,8 +38,7 @@ constexpr int TPB = B200_TPB;
 constexpr int ITEMS = B200_ITEMS;
 constexpr int TILE = TPB * ITEMS;       // 1024 pairs per tile
 static_assert(TILE <= 4096, "s_idx packs a 12-bit tile index with the bin");
-constexpr int NBIN = 8;
-constexpr int BIN_SPECIAL = 7;
+constexpr int BIN_SLOW = 7;
 
 std::atomic<int64_t> g_launches{0};
 static thread_local char g_err[256] = "";
@@ -59,46 +58,71 @@ enum : int { FN_I = 0, FN_K = 1, FN_K_PAPER = 2 };
 
 // ------------------------------------------------------------------ binning
 // bins 0..6 = E_MU, E_U4, E_U6, E_U9, E_U13, fallback split by cost (series:
-// x <= 8 / x > 8; K: Temme series x <= 2 / trapezoid x > 2); 7 = special.
-// The domain tests run on the IEEE bit patterns (integer pipe): x must lie in
-// (0, +inf), v must be finite, and for I v >= 0 (-0.0 counts as 0).
+// x <= 8 / x > 8; K: Temme series x <= 2 / trapezoid x > 2); 7 = the slow bin.
+// The fast evaluation paths (fastmath.cuh, SAFE = false) assume the operating
+// range 1e-140 <= x <= 1e140, |v| <= 1e140: there every intermediate (1/x,
+// v^2 + x^2, 1/rho, the log arguments) is a normal double.  Everything else
+// -- non-finite or out-of-domain inputs and finite arguments outside that
+// range -- goes to bin 7 and through slow_eval (library functions, rescaling).
+// The tests run on the IEEE high words (integer pipe).
 template <int FN>
 __device__ __forceinline__ int bin_of(double v, double x) {
-    const long long bx = dbits(x), bv = dbits(v);
-    const long long av = bv & 0x7FFFFFFFFFFFFFFFll;                         // |v|
-    if ((unsigned long long)(bx - 1) >= 0x7FEFFFFFFFFFFFFFull) return BIN_SPECIAL;   // x <= 0, inf, NaN
-    if (av >= 0x7FF0000000000000ll) return BIN_SPECIAL;                    // v inf / NaN
-    if (FN == FN_I && bv < 0 && av != 0) return BIN_SPECIAL;               // v < 0
-    return select_eval_bits(__longlong_as_double(av), x, av, bx, (FN == FN_I) ? 8.0 : 2.0);
+    const uint32_t hx = hiw(x), hvs = hiw(v), hv = hvs & 0x7FFFFFFFu;
+    if (hx - B200_HW_LO > B200_HW_HI - B200_HW_LO) return BIN_SLOW;    // x outside [1e-140, 1e140] (or <= 0, NaN)
+    if (hv > B200_HW_HI) return BIN_SLOW;                               // |v| > 1e140, inf, NaN
+    if (FN == FN_I && hvs != hv) return BIN_SLOW;                       // v < 0 (or -0.0: handled there)
+    return select_eval_hw(fabs(v), x, hv, hx, (FN == FN_I) ? B200_HW_X8 : B200_HW_X2);
 }
 
-// Values for the special bin: x == 0, non-finite or out-of-domain inputs.
+// The slow bin: IEEE special cases, then the full-range (SAFE) evaluation.
 template <typename T, int FN>
-__device__ __noinline__ T special_value(T v, T x) {
+__device__ __noinline__ T slow_eval(T v, T x) {
     const T nan = T(CUDART_NAN);
     if (isnan(v) || isnan(x) || x < T(0)) return nan;
     if (FN == FN_I) {
         if (v < T(0)) return nan;
         if (x == T(0)) return v == T(0) ? T(0) : T(-CUDART_INF);
         if (isinf(v)) return T(-CUDART_INF);           // I_inf(x) = 0
-        return T(CUDART_INF);                          // x = +inf
+        if (isinf(x)) return T(CUDART_INF);
+        v = fabs(v);                                   // -0.0
+        return log_iv_eval<T, true>(select_eval(double(v), double(x), B200_HW_X8), v, x);
     } else {
         if (x == T(0)) return T(CUDART_INF);           // pole
         if (isinf(v)) return T(CUDART_INF);
-        return T(-CUDART_INF);                         // x = +inf
+        if (isinf(x)) return T(-CUDART_INF);
+        v = fabs(v);
+        return log_kv_eval<T, FN == FN_K_PAPER, true>(select_eval(double(v), double(x), B200_HW_X2), v, x);
     }
 }
 
 template <typename T, int FN>
 __device__ __forceinline__ T eval_bin(int bin, T v, T x) {
-    if (bin == BIN_SPECIAL) return special_value<T, FN>(v, x);
 #ifdef B200_EVAL_NOP
-    return v + x;   // experiment only: measures the tile machinery alone
+    if (bin != BIN_SLOW) return v + x;   // experiment only: measures the tile machinery alone
 #endif
-    if (FN == FN_I) return log_iv_eval<T>(bin, v, x);
+    if (FN == FN_I) {
+        switch (bin) {
+            case E_MU: return log_bessel_mu<T, false, false>(v, x);
+            case E_U4: return log_bessel_u<T, false, 4, false>(v, x);
+            case E_U6: return log_bessel_u<T, false, 6, false>(v, x);
+            case E_U9: return log_bessel_u<T, false, 9, false>(v, x);
+            case E_U13: return log_bessel_u<T, false, 13, false>(v, x);
+            case E_FB_A:
+            case E_FB_B: return log_iv_series<T, false>(v, x);
+            default: return slow_eval<T, FN>(v, x);
+        }
+    }
     const T av = fabs(v);
-    if (FN == FN_K) return log_kv_eval<T, false>(bin, av, x);
-    return log_kv_eval<T, true>(bin, av, x);
+    switch (bin) {
+        case E_MU: return log_bessel_mu<T, true, false>(av, x);
+        case E_U4: return log_bessel_u<T, true, 4, false>(av, x);
+        case E_U6: return log_bessel_u<T, true, 6, false>(av, x);
+        case E_U9: return log_bessel_u<T, true, 9, false>(av, x);
+        case E_U13: return log_bessel_u<T, true, 13, false>(av, x);
+        case E_FB_A:
+        case E_FB_B: return FN == FN_K_PAPER ? log_kv_integral_paper<T>(av, x) : log_kv_fallback<T>(av, x);
+        default: return slow_eval<T, FN>(v, x);
+    }
 }
 
 // Counting-sort helpers.  A thread bins ITEMS <= 8 elements, so per-thread and

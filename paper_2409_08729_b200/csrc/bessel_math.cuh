@@ -51,38 +51,43 @@ __device__ __forceinline__ float d_lgamma(float a) { return lgammaf(a); }
 // ---------------------------------------------------------------- dispatch
 // Algorithm 1 / Table 1 (lines 338-352), with the
 // GPU branch set: "When running on a GPU the branches for the mu_3, U_4, U_6,
-// U_9 expressions are removed" (line 384).  Predicates read as strict
-// inequalities with natural logarithms (reading R3), decided in
-// double on both precisions (the f32 and f64 paths dispatch identically).
-// For non-negative doubles the IEEE bit pattern orders like the value, so
-// each "x > C" is one 64-bit integer compare (ALU pipe) instead of a DSETP
-// on the FP64 pipe -- the same predicate, bit for bit.
+// U_9 expressions are removed" (line 384).  Predicates are strict
+// inequalities with natural logarithms (reading R3), decided on the
+// IEEE high words of v >= 0 and x > 0 (bit order = value order for
+// non-negative doubles): "a > C" is hi(a) > HW(C), one 32-bit integer compare
+// on the ALU pipe, which is the strict inequality against C' = the largest
+// double with C's high word (C' - C < 2^-20 C, far inside the precision of
+// the fitted Table 1 constants).  Both precisions dispatch on the double value,
+// so the f32 and f64 paths choose identical methods.
 enum : int { M_MU = 0, M_U13 = 1, M_FALLBACK = 2 };
 
 __device__ __forceinline__ long long dbits(double a) { return __double_as_longlong(a); }
-#define B200_GT(a_bits, C) ((a_bits) > dbits(C))
+__device__ __forceinline__ uint32_t hiw(double a) { return uint32_t(__double2hiint(a)); }
 
 // The curved mu edge [0.5113 log x + 0.7939 > log v] is decided with the
 // hardware log2 (MUFU.LG2, fp32) and re-evaluated in double only inside a
-// 1e-4 guard band, so the result equals the double-precision predicate.
-__device__ __forceinline__ bool mu_edge(double v, double x) {
-    const float lx = __log2f(float(x)), lv = __log2f(float(v));
-    const float d = 0.5113f * lx + 1.14535832f - lv;   // 0.7939 / ln 2 = 1.14535832
-    if (fabsf(d) > 1e-4f) return d > 0.0f;
+// 1e-4 guard band (and beyond the fp32 range), so the result equals the
+// double-precision predicate.
+__device__ __forceinline__ bool mu_edge(double v, double x, uint32_t hx) {
+    if (hx <= B200_HW_X1E30) {
+        const float lx = __log2f(float(x)), lv = __log2f(float(v));
+        const float d = 0.5113f * lx + 1.14535832f - lv;   // 0.7939 / ln 2 = 1.14535832
+        if (fabsf(d) > 1e-4f) return d > 0.0f;
+    }
     return 0.5113 * log(x) + 0.7939 > log(v);
 }
 
-// v >= 0, x > 0 (callers filter the rest); bv, bx = dbits(v), dbits(x)
-__device__ __forceinline__ int select_method_bits(double v, double x, long long bv, long long bx) {
-    bool mu = B200_GT(bx, 30.0) && bv < dbits(15.3919);           // x > 30 && v < 15.3919
-    if (!mu && B200_GT(bx, 59.6925)) mu = (bv <= 0) || mu_edge(v, x);   // v <= 0 || edge
+// v >= 0, x >= 0 (callers filter the rest); hv, hx = high words
+__device__ __forceinline__ int select_method_hw(double v, double x, uint32_t hv, uint32_t hx) {
+    bool mu = hx > B200_HW_X30 && hv <= B200_HW_V15;                        // x > 30 && v < 15.3919
+    if (!mu && hx > B200_HW_X59) mu = (hv == 0) || mu_edge(v, x, hx);      // x > 59.6925 && (v <= 0 || edge)
     if (mu) return M_MU;
-    if ((B200_GT(bx, 19.6931) && B200_GT(bv, 0.7)) || B200_GT(bv, 12.6964)) return M_U13;
+    if ((hx > B200_HW_X19 && hv > B200_HW_V07) || hv > B200_HW_V12) return M_U13;
     return M_FALLBACK;
 }
 
 __device__ __forceinline__ int select_method(double v, double x) {
-    return select_method_bits(v, x, dbits(v), dbits(x));
+    return select_method_hw(v, x, hiw(v), hiw(x));
 }
 
 // Number of terms of the mu_K expansion.  The paper uses K = 20 (Table 1);
@@ -125,9 +130,9 @@ __device__ __forceinline__ T mu_series(T v, T rx) {
 }
 
 // log I = x - 1/2 log(2 pi x) + log S = x + 1/2 log(S^2 / (2 pi x))  (one log)
-template <typename T, bool IS_K>
+template <typename T, bool IS_K, bool SAFE>
 __device__ __forceinline__ T log_bessel_mu(T v, T x) {
-    if (x < Big<T>::v) {
+    if (!SAFE || x < Big<T>::v) {
         const T rx = fm_rcp(x);
         const T S = mu_series<T, IS_K>(v, rx);
         const T c = IS_K ? T(CUDART_PI / 2.0) : T(0.5 / CUDART_PI);
@@ -181,7 +186,7 @@ template <> struct EtaC<float> {
 };
 
 // vs, xs, rhos: v, x, rho scaled by the same power of two s; returns v*eta.
-template <typename T>
+template <typename T, bool SAFE>
 __device__ __forceinline__ T v_times_eta(T v, T x, T vs, T xs, T rhos, T rho) {
     // band test on z = x/v without a division: |x - z0 v| < 0.03 v
     if (fabs(fma(-EtaC<T>::hi, v, x)) < T(0.03) * v) {
@@ -194,7 +199,8 @@ __device__ __forceinline__ T v_times_eta(T v, T x, T vs, T xs, T rhos, T rho) {
         for (int k = EtaC<T>::nt - 2; k >= 0; --k) p = fma(p, d, EtaC<T>::c(k));
         return v * (p * d);
     }
-    return fma(v, fm_log_wide(xs * fm_rcp(vs + rhos)), rho);
+    const T q = xs * fm_rcp(vs + rhos);
+    return fma(v, SAFE ? fm_log_wide(q) : fm_log(q), rho);
 }
 
 // Number of U_K terms.  The paper's Table 1 fits regions for U4/U6/U9/U13 and
@@ -204,21 +210,20 @@ __device__ __forceinline__ T v_times_eta(T v, T x, T vs, T xs, T rhos, T rho) {
 // u_k(t) = t^k P_k(t^2) with sup_{t in [0,1]} |P_k| = P_k(0) =: M_k, and
 // w = t/v = 1/sqrt(v^2+x^2), so the first omitted term of U_K is at most
 // M_{K+1} w^{K+1} <= 2^-56 once sqrt(v^2+x^2) >= 1749 (K=4), 277 (K=6),
-// 77.6 (K=9) -- thresholds rounded up below (with room for the fp32 rounding
-// of rho^2, which is formed in single precision here: an upper bound test).
-__device__ __forceinline__ int select_u_terms(double v, double x) {
-    const float vf = float(v), xf = float(x);
-    const float rho2 = fmaf(vf, vf, xf * xf);
-    if (rho2 >= 1800.0f * 1800.0f) return 4;
-    if (rho2 >= 280.0f * 280.0f) return 6;
-    if (rho2 >= 80.0f * 80.0f) return 9;
+// 77.6 (K=9).  Tested on max(v, x) <= sqrt(v^2+x^2) against 1800/280/80
+// (high words): conservative, never fewer terms than the bound allows.
+__device__ __forceinline__ int select_u_terms_hw(uint32_t hv, uint32_t hx) {
+    const uint32_t m = hv > hx ? hv : hx;
+    if (m >= B200_HW_R1800) return 4;
+    if (m >= B200_HW_R280) return 6;
+    if (m >= B200_HW_R80) return 9;
     return 13;
 }
 
-template <typename T, bool IS_K, int KU>
+template <typename T, bool IS_K, int KU, bool SAFE>
 __device__ __forceinline__ T log_bessel_u(T v, T x) {
     // rescale by a power of two where v^2 + x^2 could overflow (wide-range guard)
-    const bool big = fmax(v, x) >= Big<T>::v;
+    const bool big = SAFE && fmax(v, x) >= Big<T>::v;
     const T s = big ? T(1.0 / 1267650600228229401496703205376.0) : T(1);     // 2^-100
     const T ls = big ? T(-69.31471805599453) : T(0);                         // log s
     const T vs = v * s, xs = x * s;
@@ -233,7 +238,7 @@ __device__ __forceinline__ T log_bessel_u(T v, T x) {
 #pragma unroll
     for (int k = KU - 1; k >= 1; --k) acc = fma(acc, w, uk_row<T>(k, t2));
     const T S = fabs(fma(acc, w, T(1)));
-    const T veta = v_times_eta<T>(v, x, vs, xs, rhos, rho);
+    const T veta = v_times_eta<T, SAFE>(v, x, vs, xs, rhos, rho);
     // 1/2 log(S^2 y_true c) with y_true = s y
     const T c = IS_K ? T(CUDART_PI / 2.0) : T(0.5 / CUDART_PI);
     const T tail = T(0.5) * (fm_log(S * S * y * c) + ls);
@@ -259,7 +264,7 @@ __device__ __forceinline__ T log_bessel_u(T v, T x) {
 // so sum_k b_k = N_K / P_K (one division at the end) and the stop test
 // b_k <= eps * sum reads Q_k <= eps * N_k.  In the fallback region (x <= 30,
 // v <= 12.7, at most ~45 terms) P_K < 1e130 and N_K < 1e150: no rescaling.
-template <typename T>
+template <typename T, bool SAFE>
 __device__ __forceinline__ T log_iv_series(T v, T x) {
     if (x == T(0)) return v == T(0) ? T(0) : T(-CUDART_INF);
     if constexpr (sizeof(T) == 8) {
@@ -278,7 +283,7 @@ __device__ __forceinline__ T log_iv_series(T v, T x) {
             P *= d1;
             if (Q <= N * Tr<T>::eps) break;
         }
-        const T lx = (x >= T(1e-300)) ? fm_log(T(0.5) * x) : log(T(0.5) * x);
+        const T lx = SAFE ? fm_log_wide(T(0.5) * x) : fm_log(T(0.5) * x);
         return fma(v, lx, fm_log(fm_div(N, P)) - d_lgamma(v + T(1)));
     }
     const T q = T(0.25) * x * x;
@@ -455,39 +460,39 @@ __device__ __forceinline__ T log_kv_integral_paper(T v, T x) {
 // Evaluation sub-methods (bins): the region of Algorithm 1 refined by cost.
 enum : int { E_MU = 0, E_U4 = 1, E_U6 = 2, E_U9 = 3, E_U13 = 4, E_FB_A = 5, E_FB_B = 6 };
 
-__device__ __forceinline__ int select_eval_bits(double v, double x, long long bv, long long bx, double fb_split) {
-    const int m = select_method_bits(v, x, bv, bx);
+__device__ __forceinline__ int select_eval_hw(double v, double x, uint32_t hv, uint32_t hx, uint32_t hw_split) {
+    const int m = select_method_hw(v, x, hv, hx);
     if (m == M_MU) return E_MU;
     if (m == M_U13) {
-        const int k = select_u_terms(v, x);
+        const int k = select_u_terms_hw(hv, hx);
         return k == 4 ? E_U4 : k == 6 ? E_U6 : k == 9 ? E_U9 : E_U13;
     }
-    return B200_GT(bx, fb_split) ? E_FB_B : E_FB_A;
+    return hx > hw_split ? E_FB_B : E_FB_A;
 }
-__device__ __forceinline__ int select_eval(double v, double x, double fb_split) {
-    return select_eval_bits(v, x, dbits(v), dbits(x), fb_split);
+__device__ __forceinline__ int select_eval(double v, double x, uint32_t hw_split) {
+    return select_eval_hw(v, x, hiw(v), hiw(x), hw_split);
 }
 
-template <typename T>
+template <typename T, bool SAFE>
 __device__ __forceinline__ T log_iv_eval(int e, T v, T x) {
     switch (e) {
-        case E_MU: return log_bessel_mu<T, false>(v, x);
-        case E_U4: return log_bessel_u<T, false, 4>(v, x);
-        case E_U6: return log_bessel_u<T, false, 6>(v, x);
-        case E_U9: return log_bessel_u<T, false, 9>(v, x);
-        case E_U13: return log_bessel_u<T, false, 13>(v, x);
-        default: return log_iv_series<T>(v, x);
+        case E_MU: return log_bessel_mu<T, false, SAFE>(v, x);
+        case E_U4: return log_bessel_u<T, false, 4, SAFE>(v, x);
+        case E_U6: return log_bessel_u<T, false, 6, SAFE>(v, x);
+        case E_U9: return log_bessel_u<T, false, 9, SAFE>(v, x);
+        case E_U13: return log_bessel_u<T, false, 13, SAFE>(v, x);
+        default: return log_iv_series<T, SAFE>(v, x);
     }
 }
 
-template <typename T, bool PAPER>
+template <typename T, bool PAPER, bool SAFE>
 __device__ __forceinline__ T log_kv_eval(int e, T v, T x) {
     switch (e) {
-        case E_MU: return log_bessel_mu<T, true>(v, x);
-        case E_U4: return log_bessel_u<T, true, 4>(v, x);
-        case E_U6: return log_bessel_u<T, true, 6>(v, x);
-        case E_U9: return log_bessel_u<T, true, 9>(v, x);
-        case E_U13: return log_bessel_u<T, true, 13>(v, x);
+        case E_MU: return log_bessel_mu<T, true, SAFE>(v, x);
+        case E_U4: return log_bessel_u<T, true, 4, SAFE>(v, x);
+        case E_U6: return log_bessel_u<T, true, 6, SAFE>(v, x);
+        case E_U9: return log_bessel_u<T, true, 9, SAFE>(v, x);
+        case E_U13: return log_bessel_u<T, true, 13, SAFE>(v, x);
         default: return PAPER ? log_kv_integral_paper<T>(v, x) : log_kv_fallback<T>(v, x);
     }
 }
@@ -496,7 +501,7 @@ __device__ __forceinline__ T log_kv_eval(int e, T v, T x) {
 template <typename T>
 __device__ __forceinline__ T log_iv_scalar_eval(T v, T x) {
     if (x == T(0)) return v == T(0) ? T(0) : T(-CUDART_INF);
-    return log_iv_eval<T>(select_eval(double(v), double(x), 8.0), v, x);
+    return log_iv_eval<T, true>(select_eval(double(v), double(x), B200_HW_X8), v, x);
 }
 
 }  // namespace b200

@@ -140,6 +140,21 @@ def exp_table(n: int = EXP_TAB_N):
     return out
 
 
+# Dispatch thresholds as IEEE high words (csrc/bessel_math.cuh select_*):
+# "a > C" is decided as hi(a) > HW(C), i.e. a > C' with C' the largest double
+# sharing C's high word (C' - C < 2^-20 C; reading R3).
+THRESHOLDS = {
+    "X30": 30.0, "V15": 15.3919, "X59": 59.6925, "X19": 19.6931, "V07": 0.7, "V12": 12.6964,
+    "R1800": 1800.0, "R280": 280.0, "R80": 80.0, "X8": 8.0, "X2": 2.0, "X1E30": 1e30,
+    "LO": 1e-140, "HI": 1e140,
+}
+
+
+def hiword(c: float) -> int:
+    import struct
+    return struct.unpack("<Q", struct.pack("<d", c))[0] >> 32
+
+
 def render() -> str:
     lines = [
         "// GENERATED by paper_2409_08729_b200/gen_tables.py -- do not edit.",
@@ -182,6 +197,10 @@ def render() -> str:
     lines.append("// f64 exp table: 2^(j/%d) hi, lo" % EXP_TAB_N)
     lines.append("#define B200_EXP_TAB_N %d" % EXP_TAB_N)
     lines.append("#define B200_EXPTAB_INIT_STRUCT { %s }" % ", ".join("{%.17e, %.17e}" % r for r in exp_table()))
+    lines.append("")
+    lines.append("// dispatch thresholds: IEEE high words (gen_tables.THRESHOLDS)")
+    for k, c in THRESHOLDS.items():
+        lines.append("#define B200_HW_%s 0x%08Xu   // %r" % (k, hiword(c), c))
     lines.append("")
     hi, lo, ce = eta_root_taylor()
     lines.append("// eta(z) = sqrt(1+z^2) + log(z/(1+sqrt(1+z^2))): root z0 = HI + LO and")

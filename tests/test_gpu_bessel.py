@@ -168,9 +168,17 @@ def test_classify_matches_table1(B):
     v = np.concatenate([rng.uniform(0, 200, 50_000), [1.0, 200.0, 5.0, 1.0]])
     x = np.concatenate([rng.uniform(0, 200, 50_000), [1500.0, 10.0, 5.0, 1500.0]])
     got = B.classify(_dev(v), _dev(x)).cpu().numpy()
+
+    # "a > C" is decided on IEEE high words: hi(a) > hi(C) (reading R3)
+    def hw(a):
+        return (np.asarray(a, np.float64).view(np.uint64) >> np.uint64(32)).astype(np.int64)
+
+    def gt(a, c):
+        return hw(a) > hw(c)
     with np.errstate(divide="ignore"):
-        mu = ((x > 30) & (v < 15.3919)) | ((0.5113 * np.log(x) + 0.7939 > np.log(v)) & (x > 59.6925))
-    u13 = ((x > 19.6931) & (v > 0.7)) | (v > 12.6964)
+        edge = (0.5113 * np.log(x) + 0.7939 > np.log(v)) | (hw(v) == 0)
+    mu = (gt(x, 30.0) & ~gt(v, 15.3919)) | (edge & gt(x, 59.6925))
+    u13 = (gt(x, 19.6931) & gt(v, 0.7)) | gt(v, 12.6964)
     want = np.where(mu, 0, np.where(u13, 1, 2))
     assert np.array_equal(got, want)
     assert list(got[-4:]) == [0, 1, 2, 0]     # SPEC.md dispatch examples in batch mode
