@@ -29,7 +29,10 @@ namespace b200 {
 #define B200_TPB 256
 #endif
 #ifndef B200_MINB
-#define B200_MINB 4
+#define B200_MINB 4          // CTAs per SM for log I (64 registers)
+#endif
+#ifndef B200_MINB_K
+#define B200_MINB_K 4        // CTAs per SM for log K
 #endif
 #ifndef B200_ITEMS
 #define B200_ITEMS 4
@@ -95,6 +98,20 @@ __device__ __noinline__ T slow_eval(T v, T x) {
     }
 }
 
+// mu / U bins only (bin <= E_U13)
+template <typename T, int FN>
+__device__ __forceinline__ T eval_main(int bin, T v, T x) {
+    constexpr bool K = FN != FN_I;
+    if (K) v = fabs(v);
+    switch (bin) {
+        case E_MU: return log_bessel_mu<T, K, false>(v, x);
+        case E_U4: return log_bessel_u<T, K, 4, false>(v, x);
+        case E_U6: return log_bessel_u<T, K, 6, false>(v, x);
+        case E_U9: return log_bessel_u<T, K, 9, false>(v, x);
+        default: return log_bessel_u<T, K, 13, false>(v, x);
+    }
+}
+
 template <typename T, int FN>
 __device__ __forceinline__ T eval_bin(int bin, T v, T x) {
 #ifdef B200_EVAL_NOP
@@ -142,54 +159,144 @@ __device__ __forceinline__ uint64_t shfl64(uint64_t v, int l) { return __shfl_sy
 
 static_assert(ITEMS <= 7, "8-bit warp-level bin counters hold at most 255 = 32 * 7 + 31");
 
-template <typename T, int FN>
-__global__ void __launch_bounds__(TPB, B200_MINB) bessel_eval_kernel(const T *__restrict__ vin, const T *__restrict__ xin,
-                                                          T *__restrict__ out, int64_t n) {
-    __shared__ T s_v[TILE];
-    __shared__ T s_x[TILE];
-    __shared__ T s_res[TILE];
-    __shared__ uint16_t s_idx[TILE];
-    __shared__ uint64_t s_wtot[TPB / 32];          // per-warp bin totals, 8-bit fields
-    __shared__ ulonglong2 s_off[TPB / 32];         // per-warp bin offsets, 16-bit fields
+// ------------------------------------------------------------------ async copies
+// Tiles move HBM <-> shared memory with the bulk-copy (TMA) engine: one thread
+// issues a 1-D cp.async.bulk per array, completion is tracked by an mbarrier
+// (loads) or a bulk group (stores).  Pointers that are only 8-byte aligned
+// fall back to per-thread cp.async (LDGSTS) loads and plain stores.
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t *bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "B200_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra B200_WAIT_%=;\n}" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_store(void *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void *dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(smem_u32(dst)), "l"(src), "n"(BYTES) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
+// ------------------------------------------------------------------ evaluation kernel
+// Persistent CTAs, tiles of TILE consecutive pairs, per tile:
+//   0. (one thread) start the bulk load of the NEXT tile into the other half of
+//      a double-buffered stage (v, x in tile order), so HBM reads overlap the
+//      whole current tile;
+//   1. wait for this tile's stage; every thread bins its ITEMS elements
+//      (classification only -- values stay in the stage);
+//   2. counting sort of the element indices by bin (packed 8-bit counters,
+//      warp shuffles; every warp derives its own offsets from the per-warp
+//      totals, no extra barrier);
+//   3. every warp evaluates 32 consecutive sorted slots (warp-uniform method
+//      except at <= 7 bin boundaries per tile), reading (v, x) from the stage
+//      through the index and writing the result to s_res in tile order;
+//   4. (one thread) bulk store of s_res to HBM.
+template <typename T, int FN, bool TMA>
+__global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : B200_MINB_K)
+    bessel_eval_kernel(const T *__restrict__ vin, const T *__restrict__ xin, T *__restrict__ out, int64_t n) {
+    __shared__ alignas(128) T s_stage[2][2][TILE];   // [buffer][v|x][element]
+    __shared__ alignas(128) T s_res[TILE];
+    __shared__ uint16_t s_idx[TILE];
+    __shared__ uint64_t s_wtot[TPB / 32];             // per-warp bin totals, 8-bit fields
+    __shared__ alignas(8) uint64_t s_bar[2];
+
+    constexpr int VEC = 16 / int(sizeof(T));          // elements per 16 bytes (bulk-copy granule)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t ntiles = (n + TILE - 1) / TILE;
+    auto tile_rem = [&](int64_t t) { return int(n - t * TILE < TILE ? n - t * TILE : TILE); };
 
-    // Software pipeline: the (v, x) of the next tile are loaded into registers
-    // while the current tile is binned and evaluated.
-    T nv[ITEMS], nx[ITEMS];
-    auto prefetch = [&](int64_t t) {
-        if (t >= ntiles) return;
-        const int64_t base = t * TILE;
-        const int rem = int(n - base < TILE ? n - base : TILE);
-        const T *pv = vin + base + tid, *px = xin + base + tid;
-#pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            if (tid + i * TPB < rem) {
-                nv[i] = __ldcs(pv + i * TPB);
-                nx[i] = __ldcs(px + i * TPB);
+    // stage tile t into buffer (t / gridDim.x) & 1
+    auto issue = [&](int64_t t, int buf) {
+        const int rem = tile_rem(t);
+        if constexpr (TMA) {
+            if (tid == 0) {
+                const int ra = rem & ~(VEC - 1);                  // bulk part (multiple of 16 bytes)
+                fence_proxy_async();
+                mbar_expect_tx(&s_bar[buf], uint32_t(2 * ra * sizeof(T)));
+                if (ra > 0) {
+                    bulk_load(s_stage[buf][0], vin + t * TILE, uint32_t(ra * sizeof(T)), &s_bar[buf]);
+                    bulk_load(s_stage[buf][1], xin + t * TILE, uint32_t(ra * sizeof(T)), &s_bar[buf]);
+                }
             }
+        } else {
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const int j = tid + i * TPB;
+                if (j < rem) {
+                    cp_async<sizeof(T)>(&s_stage[buf][0][j], vin + t * TILE + j);
+                    cp_async<sizeof(T)>(&s_stage[buf][1][j], xin + t * TILE + j);
+                }
+            }
+            cp_async_commit();
         }
     };
-    prefetch(blockIdx.x);
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+
+    if constexpr (TMA) {
+        if (tid == 0) {
+            mbar_init(&s_bar[0]);
+            mbar_init(&s_bar[1]);
+            fence_mbar_init();
+        }
+        __syncthreads();
+    }
+    if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    uint32_t parity[2] = {0u, 0u};
+    int buf = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= 1) {
         const int64_t base = tile * TILE;
-        const int rem = int(n - base < TILE ? n - base : TILE);
-        T lv[ITEMS], lx[ITEMS];
+        const int rem = tile_rem(tile);
+        // 0. prefetch the next tile into the other buffer (its readers finished
+        //    before the last barrier of the previous tile)
+        if (tile + gridDim.x < ntiles) issue(tile + gridDim.x, buf ^ 1);
+        // 1. wait for this tile, bin the owned elements
+        T *sv = s_stage[buf][0], *sx = s_stage[buf][1];
+        if constexpr (TMA) {
+            mbar_wait(&s_bar[buf], parity[buf]);
+            parity[buf] ^= 1u;
+            const int ra = rem & ~(VEC - 1);
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) { lv[i] = nv[i]; lx[i] = nx[i]; }
-        prefetch(tile + gridDim.x);
+            for (int i = 0; i < ITEMS; ++i) {      // the (< VEC) elements past the bulk part
+                const int j = tid + i * TPB;
+                if (j >= ra && j < rem) { sv[j] = vin[base + j]; sx[j] = xin[base + j]; }
+            }
+        } else {
+            // own copies of this tile are the older group: wait for all but the newest
+            if (tile + gridDim.x < ntiles) asm volatile("cp.async.wait_group 1;" ::: "memory");
+            else cp_async_wait_all();
+        }
         int lb[ITEMS];
         uint64_t c8 = 0;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
+            const int j = tid + i * TPB;
             lb[i] = -1;
-            if (tid + i * TPB < rem) {
-                lb[i] = bin_of<FN>(double(lv[i]), double(lx[i]));
+            if (j < rem) {
+                lb[i] = bin_of<FN>(double(sv[j]), double(sx[j]));
                 c8 += 1ull << (8 * lb[i]);
             }
         }
-        // warp-inclusive scan of the packed counts
+        // 2. warp-inclusive scan of the packed counts, per-warp totals to smem
         uint64_t incl = c8;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -198,9 +305,10 @@ __global__ void __launch_bounds__(TPB, B200_MINB) bessel_eval_kernel(const T *__
         }
         if (lane == 31) s_wtot[warp] = incl;
         __syncthreads();
-        if (warp == 0) {
-            // lanes 0..NW-1: exclusive scan over warps of the per-bin totals (16-bit
-            // fields), plus the bin bases from the tile totals (lane NW-1)
+        uint64_t plo, phi;
+        {
+            // lanes 0..NW-1 of every warp scan the per-warp totals (16-bit fields);
+            // the warp keeps the exclusive prefix of its own index
             constexpr int NW = TPB / 32;
             const uint64_t t8 = lane < NW ? s_wtot[lane] : 0ull;
             const uint64_t lo = widen_lo(t8), hi = widen_hi(t8);
@@ -213,16 +321,15 @@ __global__ void __launch_bounds__(TPB, B200_MINB) bessel_eval_kernel(const T *__
             const uint64_t tlo = shfl64(ilo, NW - 1), thi = shfl64(ihi, NW - 1);   // tile totals per bin
             // exclusive prefix over bins: field k of (x * 0x0001000100010001) is sum_{j<=k}
             constexpr uint64_t ONES = 0x0001000100010001ull;
-            const uint64_t plo = tlo * ONES;
-            const uint64_t blo = plo - tlo;                                        // bases of bins 0..3
-            const uint64_t bhi = thi * ONES - thi + (plo >> 48) * ONES;            // bases of bins 4..7
-            if (lane < NW) s_off[lane] = make_ulonglong2(blo + ilo - lo, bhi + ihi - hi);
+            const uint64_t tp = tlo * ONES;
+            const uint64_t blo = tp - tlo;                                         // bases of bins 0..3
+            const uint64_t bhi = thi * ONES - thi + (tp >> 48) * ONES;             // bases of bins 4..7
+            const uint64_t wlo = shfl64(blo + ilo - lo, warp), whi = shfl64(bhi + ihi - hi, warp);
+            // this thread's first slot per bin: warp offset + warp-exclusive count
+            const uint64_t ex8 = incl - c8;
+            plo = wlo + widen_lo(ex8);
+            phi = whi + widen_hi(ex8);
         }
-        __syncthreads();
-        // this thread's first slot per bin: warp offset + warp-exclusive count
-        const ulonglong2 wo = s_off[warp];
-        const uint64_t ex8 = incl - c8;
-        uint64_t plo = wo.x + widen_lo(ex8), phi = wo.y + widen_hi(ex8);
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
             const int b = lb[i];
@@ -231,28 +338,46 @@ __global__ void __launch_bounds__(TPB, B200_MINB) bessel_eval_kernel(const T *__
                 const uint64_t word = b < 4 ? plo : phi;
                 const int pos = int((word >> sh) & 0xFFFFull);
                 if (b < 4) plo += 1ull << sh; else phi += 1ull << sh;
-                s_v[pos] = lv[i];
-                s_x[pos] = lx[i];
                 s_idx[pos] = uint16_t((tid + i * TPB) | (b << 12));   // tile index | bin
             }
         }
+        if constexpr (TMA) {
+            if (tid == 0) bulk_wait_read();    // the previous tile's store has read s_res
+        }
         __syncthreads();
+        // 3. evaluate: sorted slot p -> element j of the stage
 #pragma unroll 1
         for (int i = 0; i < ITEMS; ++i) {
             const int p = tid + i * TPB;
             if (p < rem) {
                 const int w = s_idx[p];
-                s_res[w & 0xFFF] = eval_bin<T, FN>(w >> 12, s_v[p], s_x[p]);
+                const int j = w & 0xFFF;
+                s_res[j] = eval_bin<T, FN>(w >> 12, sv[j], sx[j]);
             }
         }
         __syncthreads();
-        // (no trailing barrier: the next tile writes shared memory only after its
-        // first barrier, which every thread reaches after this store)
-        T *po = out + base + tid;
+        // 4. store
+        if constexpr (TMA) {
+            const int ra = rem & ~(VEC - 1);
+            if (tid == 0 && ra > 0) {
+                fence_proxy_async();
+                bulk_store(out + base, s_res, uint32_t(ra * sizeof(T)));
+            }
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            if (tid + i * TPB < rem) __stcs(po + i * TPB, s_res[tid + i * TPB]);
+            for (int i = 0; i < ITEMS; ++i) {
+                const int j = tid + i * TPB;
+                if (j >= ra && j < rem) out[base + j] = s_res[j];
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const int j = tid + i * TPB;
+                if (j < rem) __stcs(out + base + j, s_res[j]);
+            }
         }
+    }
+    if constexpr (TMA) {
+        if (tid == 0) bulk_wait_all();
     }
 }
 
@@ -282,16 +407,23 @@ static int launch_eval(const T *v, const T *x, T *out, int64_t n, cudaStream_t s
     if (n < 0) return set_err(B200_ERR_INVALID_ARGUMENT, "n < 0");
     if (n == 0) return B200_OK;
     if (!v || !x || !out) return set_err(B200_ERR_INVALID_ARGUMENT, "null pointer");
-    static int occ = 0;
-    if (occ == 0) {
+    // bulk copies need 16-byte aligned global addresses
+    const bool tma = ((reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(x) |
+                       reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    static int occ[2] = {0, 0};
+    if (occ[tma] == 0) {
         int o = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, bessel_eval_kernel<T, FN>, TPB, 0);
-        occ = o > 0 ? o : 1;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &o, tma ? bessel_eval_kernel<T, FN, true> : bessel_eval_kernel<T, FN, false>, TPB, 0);
+        occ[tma] = o > 0 ? o : 1;
     }
     const int64_t ntiles = (n + TILE - 1) / TILE;
-    const int64_t resident = int64_t(device_sms()) * occ;
+    const int64_t resident = int64_t(device_sms()) * occ[tma];
     const int grid = int(ntiles < resident ? ntiles : resident);
-    bessel_eval_kernel<T, FN><<<grid, TPB, 0, s>>>(v, x, out, n);
+    if (tma)
+        bessel_eval_kernel<T, FN, true><<<grid, TPB, 0, s>>>(v, x, out, n);
+    else
+        bessel_eval_kernel<T, FN, false><<<grid, TPB, 0, s>>>(v, x, out, n);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cuda_err(cudaGetLastError(), "bessel_eval_kernel launch");
 }

@@ -310,7 +310,8 @@ __device__ __forceinline__ T log_iv_series(T v, T x) {
 // recurrence K_{nu+1} = K_{nu-1} + (2 nu / x) K_nu (stable for K) up to
 // nu = v, with the running value kept as mantissa * 10^(30 e) so nothing
 // overflows; the result is returned as a logarithm.  For 2 < x <= 30 the
-// trapezoidal rule on DLMF 10.32.9 (log_kv_trapezoid below).
+// trapezoidal rule on DLMF 10.32.9 gives K_mu, K_{mu+1} (trap_kmu below), then
+// the same recurrence.
 template <typename T>
 __device__ __forceinline__ void temme_gammas(T mu, T &gam1, T &gam2, T &gampl, T &gammi) {
     // 1/Gamma(1+z) = sum_j c_j z^j  (tables.h).  Even/odd parts give
@@ -368,53 +369,73 @@ __device__ __forceinline__ T temme_kmu(T mu, T x, T &rho) {
     }
 }
 
-// K on the band 2 < x <= 30 of the fallback region: the integral
-//   K_v(x) = int_0^inf exp(-x cosh t) cosh(v t) dt        (DLMF 10.32.9)
-// by the trapezoidal rule with step h (tables.h).  The integrand is entire and
-// decays double-exponentially, so the rule converges geometrically in 1/h
-// (error ~ exp(-2 pi d/h) for a strip of half-width d); h = 0.13 holds it
-// below 1e-16 relative on this band.  With t_k = k h,
-//   K = (h/2) e^{-x} [1 + sum_{k>=1} e^{-x (cosh t_k - 1)} (E^k + E^{-k})],  E = e^{v h},
-// all terms positive (no cancellation), at most e^{61} in size (no pivot
-// needed), one exp per node.  The integrand is unimodal in t, so the sum
-// stops once past the peak and the term is below eps of the partial sum.
-static __constant__ double c_ktrap_d[B200_KTRAP_N] = B200_KTRAP_INIT;
+// K_mu(x) and K_{mu+1}(x), |mu| <= 1/2, on the band 2 < x <= 30 of the
+// fallback region, from the integral
+//   K_nu(x) = int_0^inf exp(-x cosh t) cosh(nu t) dt        (DLMF 10.32.9)
+// by the trapezoidal rule.  The integrand is entire and decays
+// double-exponentially, so the rule converges geometrically in 1/h: the error
+// is ~ exp(-2 pi d/h) M(d) for a strip of half-width d < pi/2, with M(d)
+// growing like K_nu(x cos d) / K_nu(x).  For orders <= 3/2 the step
+// h = pi^2 / (42 + 0.8 x) keeps it below 2^-53 on 2 < x <= 30 (measured
+// largest admissible step: pi^2/(41..48 + 0.79 x)).  With
+// t_k = k h the nodes are
+//   K_nu = (h/2) e^{-x} [1 + sum_{k>=1} e^{-2x sinh^2(t_k/2)} (E_nu^k + E_nu^{-k})],  E_nu = e^{nu h},
+// sinh(t_k/2) by the three-term recurrence s_{k+1} = 2 cosh(h/2) s_k - s_{k-1}
+// (sinh grows, so the recurrence is stable), one exp per node shared by both
+// orders, all terms positive.  The integrand is unimodal in t and its first
+// node is already O(1) of the k = 0 term (2x sinh^2(h/2) < 0.4), so a term
+// below eps of the sum only occurs past the peak: stop at the first K_{mu+1}
+// term (the wider integrand) below eps of its sum.
+// Returns log K_mu and rho = K_{mu+1} / K_mu.  12-17 nodes on the band.
 template <typename T>
-__device__ __forceinline__ T log_kv_trapezoid(T v, T x) {
-    const T E = fm_exp(v * T(B200_KTRAP_H));
-    const T Ei = fm_rcp(E);
-    T ek = T(1), eik = T(1), S = T(1), prev = T(CUDART_INF);
-    for (int k = 1; k < B200_KTRAP_N; ++k) {
-        ek *= E;
-        eik *= Ei;
-        const T term = fm_exp(-x * T(c_ktrap_d[k])) * (ek + eik);
-        S += term;
-        if (term <= S * Tr<T>::eps && term <= prev) break;
-        prev = term;
+__device__ __forceinline__ T trap_kmu(T mu, T x, T &rho) {
+    const T h = T(CUDART_PI * CUDART_PI) * fm_rcp(fma(T(0.8), x, T(42)));
+    const T a = T(0.5) * h, a2 = a * a;
+    // sinh(a) and 2 cosh(a) by their Taylor series (a <= 0.12: 5 terms exact to 2^-60)
+    const T s1 = a * fma(a2 * T(1.0 / 6), fma(a2 * T(1.0 / 20), fma(a2 * T(1.0 / 42), fma(a2, T(1.0 / 72), T(1)), T(1)), T(1)), T(1));
+    const T c = fma(a2, fma(a2 * T(1.0 / 12), fma(a2 * T(1.0 / 30), fma(a2, T(1.0 / 56), T(1)), T(1)), T(1)), T(2));
+    const T Em = fm_exp(mu * h), Emi = fm_rcp(Em);
+    const T eh = fm_exp(h), ehi = fm_rcp(eh);
+    const T Ep = Em * eh, Epi = Emi * ehi;
+    T pm = T(1), pmi = T(1), pp = T(1), ppi = T(1);
+    T A = T(1), B = T(1), sp = T(0), sk = s1;
+    const T m2x = T(-2) * x;
+#pragma unroll 2
+    for (int k = 1; k < 64; ++k) {
+        const T e = fm_exp_nc(m2x * sk * sk);
+        pm *= Em; pmi *= Emi; pp *= Ep; ppi *= Epi;
+        const T tb = e * (pp + ppi);
+        A = fma(e, pm + pmi, A);
+        B += tb;
+        if (tb <= B * Tr<T>::eps) break;
+        const T sn = fma(c, sk, -sp);
+        sp = sk;
+        sk = sn;
     }
-    return -x + fm_log(T(0.5 * B200_KTRAP_H) * S);
+    rho = B * fm_rcp(A);
+    return -x + fm_log(T(0.5) * h * A);
 }
 
 template <typename T>
 __device__ __forceinline__ T log_kv_fallback(T v, T x) {
-    if (x > T(2)) return log_kv_trapezoid<T>(v, x);
     const int nl = int(floor(v + T(0.5)));
     const T mu = v - T(nl);
     T rho;
-    const T lk = temme_kmu<T>(mu, x, rho);
+    const T lk = (x > T(2)) ? trap_kmu<T>(mu, x, rho) : temme_kmu<T>(mu, x, rho);
     if (nl == 0) return lk;
-    // forward recurrence on K_{mu+i} / K_mu, scaled by 2^-e
+    // forward recurrence K_{nu+1} = K_{nu-1} + (2 nu / x) K_nu on K_{mu+i} / K_mu,
+    // scaled by 10^-30 whenever it exceeds 10^30 (only possible for small x)
     T km = T(1), kp = rho;
-    const T two_over_x = T(2) / x;
+    const T two_over_x = T(2) * fm_rcp(x);
     int e = 0;
-    for (int i = 1; i <= nl; ++i) {
+    for (int i = 1; i < nl; ++i) {
         const T kn = fma((mu + T(i)) * two_over_x, kp, km);
         km = kp;
         kp = kn;
         if (kp > T(1e30)) { km *= T(1e-30); kp *= T(1e-30); e += 1; }
     }
-    // after nl steps km = K_v / K_mu * 1e-30^e
-    return lk + log(km) + T(e) * T(69.07755278982137);   // 30 ln 10
+    // after nl - 1 steps kp = K_v / K_mu * 1e-30^e
+    return lk + fm_log(kp) + T(e) * T(69.07755278982137);   // 30 ln 10
 }
 
 // ---------------------------------------------------------------- paper K

@@ -83,6 +83,23 @@ __device__ __forceinline__ double fm_exp(double y) {
     return __hiloint2double(__double2hiint(res) + ((k >> 6) << 20), __double2loint(res));
 }
 
+// exp(y) for -708 <= y <= 709 without the clamp (caller guarantees the range).
+__device__ __forceinline__ double fm_exp_nc(double y) {
+    constexpr double SHIFT = 6755399441055744.0;
+    double kd = fma(y, c_fm.exp_inv, SHIFT);
+    const int k = __double2loint(kd);
+    kd -= SHIFT;
+    double r = fma(kd, -c_fm.exp_chi, y);
+    r = fma(kd, -c_fm.exp_clo, r);
+    double p = fma(r, c_fm.exp_c5, c_fm.exp_c4);
+    p = fma(p, r, c_fm.exp_c3);
+    p = fma(p, r, 0.5);
+    p = fma(p, r * r, r);
+    const double2 T = __ldg(&g_exptab[k & (B200_EXP_TAB_N - 1)]);
+    const double res = T.x + fma(T.x, p, T.y);
+    return __hiloint2double(__double2hiint(res) + ((k >> 6) << 20), __double2loint(res));
+}
+
 // 1/a for finite normal |a| in [2^-1000, 2^1000].
 __device__ __forceinline__ double fm_rcp(double a) {
     double r;
@@ -117,6 +134,7 @@ __device__ __forceinline__ double fm_log_wide(double a) { return a >= 1e-300 ? f
 __device__ __forceinline__ float fm_log_wide(float a) { return logf(a); }
 __device__ __forceinline__ float fm_log(float a) { return logf(a); }
 __device__ __forceinline__ float fm_exp(float y) { return expf(y); }
+__device__ __forceinline__ float fm_exp_nc(float y) { return expf(y); }
 __device__ __forceinline__ float fm_rcp(float a) { return __frcp_rn(a); }
 __device__ __forceinline__ float fm_div(float x, float y) { return x / y; }
 __device__ __forceinline__ float fm_rsqrt(float a) { return rsqrtf(a); }

@@ -15,10 +15,8 @@ writes ``csrc/tables.h``.  Deterministic: regenerating yields identical bytes
 * 1/Gamma(1+z) Taylor coefficients -- used by the K fallback (Temme's series,
   DESIGN.md §K-fallback), computed with mpmath at 60 digits.
 
-* cosh(k h) - 1, k = 0..KTRAP_N-1 -- nodes of the trapezoidal rule for
-  K_v(x) = int_0^inf exp(-x cosh t) cosh(v t) dt (DLMF 10.32.9) on the K
-  fallback band 2 < x <= 30, as 2 sinh^2(k h / 2) (no
-  cancellation), mpmath at 60 digits.
+* f64 log / exp tables of csrc/fastmath.cuh and the IEEE high words of the
+  dispatch thresholds.
 """
 from __future__ import annotations
 
@@ -81,20 +79,6 @@ def eta_root_taylor(nterms: int = ETA_TERMS):
     lo = float(z0 - mpmath.mpf(hi))
     c = mpmath.taylor(eta, z0, nterms)
     return hi, lo, [float(ci) for ci in c[1:]]
-
-
-# Trapezoid step for the K fallback band: the discretisation
-# error of the trapezoidal rule on this analytic integrand decays like
-# exp(-2 pi d / h) (d = half-width of the strip of analyticity used); on
-# 2 < x <= 30, 0 <= v <= 12.7 h = 0.13 keeps it below 1e-16 relative.
-KTRAP_H = 0.13
-KTRAP_N = 48
-
-
-def ktrap_nodes(h: float = KTRAP_H, n: int = KTRAP_N):
-    import mpmath
-    mpmath.mp.dps = 60
-    return [float(2 * mpmath.sinh(mpmath.mpf(k) * mpmath.mpf(h) / 2) ** 2) for k in range(n)]
 
 
 # Table-driven f64 log/exp of csrc/fastmath.cuh.
@@ -183,11 +167,6 @@ def render() -> str:
     lines.append("")
     lines.append("// 1/k, k = 0..400 (entry 0 unused)")
     lines.append("#define B200_INV_INIT { 0.0, %s }" % ", ".join("%.17e" % (1.0 / k) for k in range(1, 401)))
-    lines.append("")
-    lines.append("// K fallback trapezoid (DESIGN.md §5): step h and cosh(k h) - 1, k = 0..N-1")
-    lines.append("#define B200_KTRAP_H %r" % KTRAP_H)
-    lines.append("#define B200_KTRAP_N %d" % KTRAP_N)
-    lines.append("#define B200_KTRAP_INIT { %s }" % ", ".join("%.17e" % c for c in ktrap_nodes()))
     lines.append("")
     lines.append("// f64 log table (csrc/fastmath.cuh): {1/c_i, -log(1/c_i) hi, lo, 0}, i = 0..%d" % ((1 << LOG_TAB_BITS) - 1))
     lines.append("#define B200_LOG_TAB_BITS %d" % LOG_TAB_BITS)
