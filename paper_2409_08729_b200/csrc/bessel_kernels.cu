@@ -275,10 +275,12 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : B200_MINB_K)
             mbar_wait(&s_bar[buf], parity[buf]);
             parity[buf] ^= 1u;
             const int ra = rem & ~(VEC - 1);
-#pragma unroll
-            for (int i = 0; i < ITEMS; ++i) {      // the (< VEC) elements past the bulk part
-                const int j = tid + i * TPB;
-                if (j >= ra && j < rem) { sv[j] = vin[base + j]; sx[j] = xin[base + j]; }
+            if (ra != rem) {                       // the (< VEC) elements past the bulk part,
+#pragma unroll                                     // loaded by the thread that bins them
+                for (int i = 0; i < ITEMS; ++i) {
+                    const int j = tid + i * TPB;
+                    if (j >= ra && j < rem) { sv[j] = vin[base + j]; sx[j] = xin[base + j]; }
+                }
             }
         } else {
             // own copies of this tile are the older group: wait for all but the newest
@@ -363,11 +365,7 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : B200_MINB_K)
                 fence_proxy_async();
                 bulk_store(out + base, s_res, uint32_t(ra * sizeof(T)));
             }
-#pragma unroll
-            for (int i = 0; i < ITEMS; ++i) {
-                const int j = tid + i * TPB;
-                if (j >= ra && j < rem) out[base + j] = s_res[j];
-            }
+            if (ra != rem && tid < rem - ra) out[base + ra + tid] = s_res[ra + tid];
         } else {
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {

@@ -400,17 +400,19 @@ __device__ __forceinline__ T trap_kmu(T mu, T x, T &rho) {
     T pm = T(1), pmi = T(1), pp = T(1), ppi = T(1);
     T A = T(1), B = T(1), sp = T(0), sk = s1;
     const T m2x = T(-2) * x;
-#pragma unroll 2
-    for (int k = 1; k < 64; ++k) {
-        const T e = fm_exp_nc(m2x * sk * sk);
+    for (int k = 1; k < 64; k += 2) {     // two nodes per trip, stop test on the second
+        const T s2 = fma(c, sk, -sp);
+        const T e1 = fm_exp_nc(m2x * sk * sk), e2 = fm_exp_nc(m2x * s2 * s2);
         pm *= Em; pmi *= Emi; pp *= Ep; ppi *= Epi;
-        const T tb = e * (pp + ppi);
-        A = fma(e, pm + pmi, A);
+        A = fma(e1, pm + pmi, A);
+        B = fma(e1, pp + ppi, B);
+        pm *= Em; pmi *= Emi; pp *= Ep; ppi *= Epi;
+        const T tb = e2 * (pp + ppi);
+        A = fma(e2, pm + pmi, A);
         B += tb;
         if (tb <= B * Tr<T>::eps) break;
-        const T sn = fma(c, sk, -sp);
-        sp = sk;
-        sk = sn;
+        sp = s2;
+        sk = fma(c, s2, -sk);
     }
     rho = B * fm_rcp(A);
     return -x + fm_log(T(0.5) * h * A);
@@ -421,20 +423,34 @@ __device__ __forceinline__ T log_kv_fallback(T v, T x) {
     const int nl = int(floor(v + T(0.5)));
     const T mu = v - T(nl);
     T rho;
-    const T lk = (x > T(2)) ? trap_kmu<T>(mu, x, rho) : temme_kmu<T>(mu, x, rho);
+    const T tox = T(2) * fm_rcp(x);
+    // forward recurrence K_{nu+1} = K_{nu-1} + (2 nu / x) K_nu (stable for K)
+    // on the ratios K_{mu+i} / K_mu, from i = 0, 1 up to i = nl
+    if (x > T(2)) {
+        const T lk = trap_kmu<T>(mu, x, rho);
+        // x > 2, v <= 12.7: K_v / K_mu < 1e12, no rescaling needed
+        T km = T(1), kp = rho, nu = mu;
+        for (int i = 1; i < nl; ++i) {
+            nu += T(1);
+            const T kn = fma(nu * tox, kp, km);
+            km = kp;
+            kp = kn;
+        }
+        return nl == 0 ? lk : lk + fm_log(kp);
+    }
+    const T lk = temme_kmu<T>(mu, x, rho);
     if (nl == 0) return lk;
-    // forward recurrence K_{nu+1} = K_{nu-1} + (2 nu / x) K_nu on K_{mu+i} / K_mu,
-    // scaled by 10^-30 whenever it exceeds 10^30 (only possible for small x)
-    T km = T(1), kp = rho;
-    const T two_over_x = T(2) * fm_rcp(x);
+    // small x: scaled by 10^-30 whenever the ratio exceeds 10^30
+    T km = T(1), kp = rho, nu = mu;
     int e = 0;
     for (int i = 1; i < nl; ++i) {
-        const T kn = fma((mu + T(i)) * two_over_x, kp, km);
+        nu += T(1);
+        const T kn = fma(nu * tox, kp, km);
         km = kp;
         kp = kn;
         if (kp > T(1e30)) { km *= T(1e-30); kp *= T(1e-30); e += 1; }
     }
-    // after nl - 1 steps kp = K_v / K_mu * 1e-30^e
+    // kp = K_v / K_mu * 1e-30^e
     return lk + fm_log(kp) + T(e) * T(69.07755278982137);   // 30 ln 10
 }
 
