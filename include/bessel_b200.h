@@ -57,7 +57,9 @@ int b200_log_iv_f32(const float *v_d, const float *x_d, float *out_d, int64_t n,
 /* ------------------------------------------------------------------------
  * log K_v(x) -- PAPER.md §3.2 (Eqs. (log Kv mu k), (log Kv u k), lines 233-246)
  * by Algorithm 1; the small-argument fallback replaces the paper's Simpson
- * integral (line 251-269) by Temme's method, see DESIGN.md §K-fallback.
+ * integral (line 251-269) by the trapezoidal rule on the same integral
+ * representation (2 < x <= 30) or Temme's series (x <= 2), each followed by
+ * the forward recurrence in the order -- DESIGN.md §5.
  *   Domain: x > 0, any real v (K_{-v} = K_v).  x = 0 -> +inf (pole);
  *   x < 0 or NaN input -> NaN.
  */

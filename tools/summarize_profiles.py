@@ -121,7 +121,7 @@ def main():
     if "--promote" in sys.argv and os.path.exists(os.path.join(dst, "ncu_full.json")):
         counts = {}
         for e in json.load(open(os.path.join(dst, "ncu_full.json"))):
-            m = re.search(r"bessel_eval_kernel<double, (?:\(int\))?(\d)>", e["kernel"])
+            m = re.search(r"bessel_eval_kernel<double, (?:\(int\))?(\d)[,>]", e["kernel"])
             fn = {"0": "log_iv", "1": "log_kv"}.get(m.group(1)) if m else None
             if fn and "double" in e["kernel"] and "bessel_eval_kernel" in e["kernel"] and e.get("fp64_flop_per_eval"):
                 counts[fn] = {"fp64_flop_per_eval": e["fp64_flop_per_eval"],
