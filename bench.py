@@ -3,9 +3,11 @@
 
 Workload (BASELINE.json configs[1] + configs[2]): per GPU, the paper's SciPy
 comparison grid -- v in {2^0..2^10}, 20M x per v uniform in [1, 100]
-(220M pairs, Fig. 1 caption).  One step = b200_log_iv_f64 over the
-whole grid followed by b200_log_kv_f64 over the same grid (440M evaluations).
-Inputs (3.5 GB) and outputs live in HBM, far larger than L2.
+(220M pairs, Fig. 1 caption).  One step = log I_v(x) and log K_v(x)
+of every pair (440M evaluations) in one fused pass, b200_log_ivkv_f64; the
+same work as two calls (b200_log_iv_f64 then b200_log_kv_f64) is timed beside
+it and reported as "separate_calls".  Inputs (3.5 GB) and outputs (3.5 GB)
+live in HBM, far larger than L2.
 
 Multi-GPU: one process per GPU (torchrun), every rank evaluates its own
 220M-pair batch (weak scaling, no data-path collective); time = max over ranks.
@@ -31,7 +33,7 @@ METRIC = "logIv/logKv Gevals/s fp64"
 UNIT = "Gevals/s"
 N_PER_V = 20_000_000
 N_ORDERS = 11
-BYTES_PER_EVAL = 24          # read v, x (2 x 8 B), write out (8 B)  -- DESIGN.md §Roofline
+BYTES_PER_PAIR = 32          # read v, x (2 x 8 B), write log I, log K (2 x 8 B)  -- DESIGN.md §6
 # FP64 operations (DADD + DMUL + 2*DFMA, thread level) and DRAM bytes per
 # evaluation of the dominant kernel, from the ncu --set full capture of the
 # bench workload promoted to profiles/roofline_counts.json
@@ -177,6 +179,29 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _timed(step, steps, stream, dist):
+    """CUDA-event time of `steps` calls of step() on `stream`, bracketed by a barrier and a
+    device synchronize on both sides; max over ranks."""
+    import torch
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        step()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    ms = t0.elapsed_time(t1)
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device=torch.device("cuda", torch.cuda.current_device()))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    return ms
+
+
 def run_ours(args):
     import torch
 
@@ -195,114 +220,116 @@ def run_ours(args):
     out_i = torch.empty_like(v)
     out_k = torch.empty_like(v)
     stream = torch.cuda.current_stream(dev)
+    evals_per_step = 2 * n * ws
 
-    def step(ev=None):
-        if ev is not None:
-            ev[0].record(stream)
-        B.log_iv(v, x, out=out_i)
-        if ev is not None:
-            ev[1].record(stream)
-        B.log_kv(v, x, out=out_k)
-        if ev is not None:
-            ev[2].record(stream)
+    # ---- the step: log I_v(x) and log K_v(x) of every pair, one fused pass (b200_log_ivkv_f64)
+    def step():
+        B.log_ivkv(v, x, out_i, out_k)
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     # non-finite guard on the warm-up outputs (the method never produces inf/NaN here)
     nonfinite = int((~torch.isfinite(out_i)).sum().item() + (~torch.isfinite(out_k)).sum().item())
-
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     clocks = Clocks(lrank) if rank == 0 else None
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
     launches0 = B.launch_count()
-    t_start = torch.cuda.Event(enable_timing=True)
-    t_end = torch.cuda.Event(enable_timing=True)
-    t_start.record(stream)
-    for s in range(args.steps):
-        step(evs[s])
-    t_end.record(stream)
-    torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
+    ms = _timed(step, args.steps, stream, dist)
     launches = B.launch_count() - launches0
     clk = clocks.stop() if clocks else None
-    ms = t_start.elapsed_time(t_end)
-    ms_i = sum(e[0].elapsed_time(e[1]) for e in evs) / args.steps
-    ms_k = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
-    if dist:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-
-    evals_per_step = 2 * n * ws
     value = evals_per_step * args.steps / (ms / 1e3) / 1e9
 
-    # ---- end to end through the C ABI with pinned HOST buffers (H2D + kernels + D2H timed)
+    # ---- the same work as two separate calls (b200_log_iv_f64, then b200_log_kv_f64)
+    sep = None
+    if not args.skip_separate:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        acc = [0.0, 0.0]
+
+        def step_sep():
+            ev[0].record(stream)
+            B.log_iv(v, x, out=out_i)
+            ev[1].record(stream)
+            B.log_kv(v, x, out=out_k)
+            ev[2].record(stream)
+
+        def step_sep_acc():
+            step_sep()
+            torch.cuda.synchronize()
+            acc[0] += ev[0].elapsed_time(ev[1])
+            acc[1] += ev[1].elapsed_time(ev[2])
+        for _ in range(args.warmup):
+            step_sep()
+        ms_sep = _timed(step_sep, args.steps, stream, dist)
+        for _ in range(args.steps):
+            step_sep_acc()
+        sep = {"value": evals_per_step * args.steps / (ms_sep / 1e3) / 1e9, "unit": UNIT,
+               "ms_per_step": ms_sep / args.steps,
+               "kernel_ms": {"log_iv": acc[0] / args.steps, "log_kv": acc[1] / args.steps},
+               "note": "b200_log_iv_f64 then b200_log_kv_f64 over the same grid (2 launches per step)"}
+
+    # ---- end to end through the C ABI with pinned HOST buffers (H2D + kernel + D2H timed)
     e2e = None
     if not args.skip_e2e:
         vh = v.cpu().pin_memory()
         xh = x.cpu().pin_memory()
         oi = torch.empty_like(vh, pin_memory=True)
         ok = torch.empty_like(vh, pin_memory=True)
-        B.log_iv_host(vh, xh, oi)
-        B.log_kv_host(vh, xh, ok)
+        B.log_ivkv_host(vh, xh, oi, ok)
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
         reps = max(1, min(args.steps, 3))
         for _ in range(reps):
-            B.log_iv_host(vh, xh, oi)
-            B.log_kv_host(vh, xh, ok)
+            B.log_ivkv_host(vh, xh, oi, ok)
         te = time.perf_counter() - t0
         if dist:
             t = torch.tensor([te], dtype=torch.float64, device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             te = float(t.item())
         e2e = {"value": evals_per_step * reps / te / 1e9, "unit": UNIT,
-               "h2d_bytes_per_step": 2 * 2 * n * 8, "d2h_bytes_per_step": 2 * n * 8,
-               "note": "b200_log_iv_f64_host + b200_log_kv_f64_host on pinned host arrays; "
-                       "chunked H2D/kernel/D2H pipeline; host wall clock"}
+               "h2d_bytes_per_step": 2 * n * 8, "d2h_bytes_per_step": 2 * n * 8,
+               "note": "b200_log_ivkv_f64_host on pinned host arrays: v, x cross PCIe once per pair, "
+                       "both results come back; chunked H2D/kernel/D2H pipeline on 3 streams; host wall clock"}
         del vh, xh, oi, ok
 
     if rank != 0:
         return
     hbm_peak, hbm_src = _peaks()
-    dom, dom_ms = ("log_kv", ms_k) if ms_k >= ms_i else ("log_iv", ms_i)
-    gbs = BYTES_PER_EVAL * n / (dom_ms / 1e3) / 1e9
+    kms = ms / args.steps                      # one launch per step: the step is the kernel
+    gbs = BYTES_PER_PAIR * n / (kms / 1e3) / 1e9
     roof = {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s", "frac": gbs / hbm_peak,
-            "traffic": None, "kernel": f"bessel_eval_kernel ({dom})", "peak_source": hbm_src,
-            "kernel_ms": dom_ms}
+            "traffic": None, "kernel": "bessel_eval_kernel<double, FN_IK> (b200_log_ivkv_f64)",
+            "peak_source": hbm_src, "kernel_ms": kms}
     fp64_peak, fp64_src = _fp64_peak()
-    cnt = _roofline_counts().get(dom, {})
-    fl = cnt.get("fp64_flop_per_eval")
+    cnt = _roofline_counts().get("log_ivkv", {})
+    fl = cnt.get("fp64_flop_per_eval")         # per pair (two evaluations)
     if cnt.get("dram_bytes_per_eval"):
-        roof["traffic"] = cnt["dram_bytes_per_eval"] * n
-        roof["traffic_source"] = cnt["source"] + ", scaled per evaluation to this launch"
+        roof["traffic"] = cnt["dram_bytes_per_eval"]
+        roof["traffic_source"] = cnt["source"] + "; DRAM bytes per pair (ncu), algorithmic: 32"
     if fl and fp64_peak:
-        tf = fl * n / (dom_ms / 1e3) / 1e12
+        tf = fl * n / (kms / 1e3) / 1e12
         if tf / fp64_peak > gbs / hbm_peak:
             roof = {"bound": "alu", "achieved": tf, "peak": fp64_peak, "unit": "TFLOP/s",
                     "frac": tf / fp64_peak, "traffic": roof.get("traffic"),
-                    "kernel": f"bessel_eval_kernel ({dom})", "peak_source": fp64_src,
-                    "kernel_ms": dom_ms, "fp64_flop_per_eval": fl, "flop_source": cnt["source"],
+                    "traffic_source": roof.get("traffic_source"),
+                    "kernel": "bessel_eval_kernel<double, FN_IK> (b200_log_ivkv_f64)",
+                    "peak_source": fp64_src, "kernel_ms": kms, "fp64_flop_per_pair": fl,
+                    "flop_source": cnt["source"] + " (DADD + DMUL + 2 DFMA executed per pair)",
                     "hbm": {"achieved_gbs": gbs, "peak_gbs": hbm_peak, "frac": gbs / hbm_peak,
-                            "algorithmic_bytes_per_eval": BYTES_PER_EVAL}}
+                            "algorithmic_bytes_per_pair": BYTES_PER_PAIR}}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"log I_v and log K_v over v in {{2^0..2^10}} x {n_per_v} x~U[1,100] per GPU "
-                               f"({n} pairs, v-major; configs[1]+configs[2])",
+        "config": {"workload": f"log I_v and log K_v of every pair of v in {{2^0..2^10}} x {n_per_v} "
+                               f"x~U[1,100] per GPU ({n} pairs, v-major; configs[1]+configs[2]), "
+                               "one fused pass (b200_log_ivkv_f64)",
                    "pairs_per_gpu": n, "evals_per_step": evals_per_step,
                    "l2": "inputs_larger_than_l2 (3.5 GB in, 3.5 GB out per step)",
                    "parallelism": f"dp{ws} (contiguous batch per rank, no collective)"},
-        "kernel_ms": {"log_iv": ms_i, "log_kv": ms_k},
         "roofline": roof,
         "gpu_launches": launches,
         "nonfinite_outputs": nonfinite,
+        "separate_calls": sep,
         "e2e": e2e,
         "clocks": clk,
     }
@@ -319,6 +346,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n-per-v", type=int, default=N_PER_V)
     ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-separate", action="store_true")
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()

@@ -66,6 +66,21 @@ int b200_log_iv_f32(const float *v_d, const float *x_d, float *out_d, int64_t n,
 int b200_log_kv_f64(const double *v_d, const double *x_d, double *out_d, int64_t n, void *stream);
 int b200_log_kv_f32(const float *v_d, const float *x_d, float *out_d, int64_t n, void *stream);
 
+/* ------------------------------------------------------------------------
+ * log I_v(x) AND log K_v(x) of the same pairs in one pass (fused): the inputs
+ * are read once, classification / binning is shared, and inside the mu and U
+ * regions the expansions share every term (I and K differ only by the sign
+ * pattern (-1)^k, Eqs. (log Iv mu k)/(log Kv mu k), (log Iv u k)/(log Kv u k)).
+ *   out_i_d[i] = log I_{v_i}(x_i), out_k_d[i] = log K_{v_i}(x_i), with the
+ *   domains and special values of the two functions above (v < 0: out_i NaN,
+ *   out_k = log K_{|v|}).  Results equal the separate calls to the stated
+ *   accuracy (not bit for bit: the fused sums round differently).
+ */
+int b200_log_ivkv_f64(const double *v_d, const double *x_d, double *out_i_d, double *out_k_d, int64_t n,
+                      void *stream);
+int b200_log_ivkv_f32(const float *v_d, const float *x_d, float *out_i_d, float *out_k_d, int64_t n,
+                      void *stream);
+
 /* The paper's own K fallback (log-domain Rothwell integral, Simpson N=600,
  * heuristic maxima) on the same dispatch -- kept for
  * fidelity studies; accuracy is the paper's (~1e-9, Table 2), not 1e-13. */
@@ -82,6 +97,7 @@ int b200_classify_f64(const double *v_d, const double *x_d, int8_t *method_d, in
  */
 int b200_log_iv_f64_host(const double *v_h, const double *x_h, double *out_h, int64_t n);
 int b200_log_kv_f64_host(const double *v_h, const double *x_h, double *out_h, int64_t n);
+int b200_log_ivkv_f64_host(const double *v_h, const double *x_h, double *out_i_h, double *out_k_h, int64_t n);
 
 /* ------------------------------------------------------------------------
  * von Mises-Fisher fit, §6.3 (lines 663-693).

@@ -19,7 +19,7 @@ from ._build import build as build_library  # noqa: F401
 from ._lib import B200Error, check, launch_count, lib  # noqa: F401
 
 __all__ = [
-    "log_iv", "log_kv", "log_kv_paper", "classify", "log_iv_host", "log_kv_host",
+    "log_iv", "log_kv", "log_ivkv", "log_kv_paper", "classify", "log_iv_host", "log_kv_host", "log_ivkv_host",
     "vmf_colsum", "vmf_fit_from_colsum", "vmf_fit", "VMF_STATS", "B200Error",
     "launch_count", "METHOD_MU", "METHOD_U13", "METHOD_FALLBACK",
 ]
@@ -70,6 +70,19 @@ def log_kv(v: torch.Tensor, x: torch.Tensor, out: torch.Tensor | None = None) ->
     return _call("b200_log_kv_f64", "b200_log_kv_f32", v, x, out)
 
 
+def log_ivkv(v: torch.Tensor, x: torch.Tensor, out_i: torch.Tensor | None = None,
+             out_k: torch.Tensor | None = None):
+    """(log I_v(x), log K_v(x)) of the same pairs in one fused pass (shared loads, dispatch,
+    and expansion terms); float64 or float32 CUDA tensors."""
+    v, x, out_i = _pair(v, x, out_i)
+    _, _, out_k = _pair(v, x, out_k)
+    fn = lib().b200_log_ivkv_f64 if v.dtype == torch.float64 else lib().b200_log_ivkv_f32
+    with torch.cuda.device(v.device):
+        check(fn(v.data_ptr(), x.data_ptr(), out_i.data_ptr(), out_k.data_ptr(), v.numel(), _stream(v)),
+              fn.__name__)
+    return out_i, out_k
+
+
 def log_kv_paper(v: torch.Tensor, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     """log K_v(x) with the paper's own Simpson-integral fallback (float64 only)."""
     if v.dtype != torch.float64:
@@ -117,6 +130,30 @@ def log_iv_host(v, x, out=None):
 def log_kv_host(v, x, out=None):
     """log K_v(x) for HOST float64 arrays (pinned torch tensors or numpy); staged through the GPU."""
     return _host_call("b200_log_kv_f64_host", v, x, out)
+
+
+def log_ivkv_host(v, x, out_i=None, out_k=None):
+    """(log I_v(x), log K_v(x)) for HOST float64 arrays in one fused pass: the inputs cross
+    PCIe once for both functions."""
+    if isinstance(v, torch.Tensor):
+        if v.is_cuda or x.is_cuda or v.dtype != torch.float64 or x.dtype != torch.float64:
+            raise TypeError("host variants take float64 CPU tensors or numpy arrays")
+        v, x = v.contiguous(), x.contiguous()
+        if v.shape != x.shape:
+            raise ValueError("v and x must have the same shape")
+        out_i = torch.empty_like(v, pin_memory=v.is_pinned()) if out_i is None else out_i
+        out_k = torch.empty_like(v, pin_memory=v.is_pinned()) if out_k is None else out_k
+        ptrs = (v.data_ptr(), x.data_ptr(), out_i.data_ptr(), out_k.data_ptr(), v.numel())
+    else:
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        if v.shape != x.shape:
+            raise ValueError("v and x must have the same shape")
+        out_i = np.empty_like(v) if out_i is None else out_i
+        out_k = np.empty_like(v) if out_k is None else out_k
+        ptrs = (v.ctypes.data, x.ctypes.data, out_i.ctypes.data, out_k.ctypes.data, v.size)
+    check(lib().b200_log_ivkv_f64_host(*ptrs), "b200_log_ivkv_f64_host")
+    return out_i, out_k
 
 
 # ------------------------------------------------------------------ vMF

@@ -57,7 +57,7 @@ static int cuda_err(cudaError_t e, const char *where) {
 }
 
 // Function ids
-enum : int { FN_I = 0, FN_K = 1, FN_K_PAPER = 2 };
+enum : int { FN_I = 0, FN_K = 1, FN_K_PAPER = 2, FN_IK = 3 };   // FN_IK: both, one pass
 
 // ------------------------------------------------------------------ binning
 // bins 0..6 = E_MU, E_U4, E_U6, E_U9, E_U13, fallback split by cost (series:
@@ -73,7 +73,7 @@ __device__ __forceinline__ int bin_of(double v, double x) {
     const uint32_t hx = hiw(x), hvs = hiw(v), hv = hvs & 0x7FFFFFFFu;
     if (hx - B200_HW_LO > B200_HW_HI - B200_HW_LO) return BIN_SLOW;    // x outside [1e-140, 1e140] (or <= 0, NaN)
     if (hv > B200_HW_HI) return BIN_SLOW;                               // |v| > 1e140, inf, NaN
-    if (FN == FN_I && hvs != hv) return BIN_SLOW;                       // v < 0 (or -0.0: handled there)
+    if ((FN == FN_I || FN == FN_IK) && hvs != hv) return BIN_SLOW;     // v < 0 (or -0.0: handled there)
     return select_eval_hw(fabs(v), x, hv, hx, (FN == FN_I) ? B200_HW_X8 : B200_HW_X2);
 }
 
@@ -139,6 +139,29 @@ __device__ __forceinline__ T eval_bin(int bin, T v, T x) {
         case E_FB_A:
         case E_FB_B: return FN == FN_K_PAPER ? log_kv_integral_paper<T>(av, x) : log_kv_fallback<T>(av, x);
         default: return slow_eval<T, FN>(v, x);
+    }
+}
+
+// Fused I + K: both results of one element (bins as for K, v >= 0 or slow).
+template <typename T>
+__device__ __forceinline__ void eval_bin_ik(int bin, T v, T x, T &ri, T &rk) {
+#ifdef B200_EVAL_NOP
+    if (bin != BIN_SLOW) { ri = v + x; rk = v - x; return; }
+#endif
+    switch (bin) {
+        case E_MU: log_bessel_mu_ik<T>(v, x, ri, rk); break;
+        case E_U4: log_bessel_u_ik<T, 4>(v, x, ri, rk); break;
+        case E_U6: log_bessel_u_ik<T, 6>(v, x, ri, rk); break;
+        case E_U9: log_bessel_u_ik<T, 9>(v, x, ri, rk); break;
+        case E_U13: log_bessel_u_ik<T, 13>(v, x, ri, rk); break;
+        case E_FB_A:
+        case E_FB_B:
+            ri = log_iv_series<T, false>(v, x);
+            rk = log_kv_fallback<T>(v, x);
+            break;
+        default:
+            ri = slow_eval<T, FN_I>(v, x);
+            rk = slow_eval<T, FN_K>(v, x);
     }
 }
 
@@ -212,12 +235,19 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 //      except at <= 7 bin boundaries per tile), reading (v, x) from the stage
 //      through the index and writing the result to s_res in tile order;
 //   4. (one thread) bulk store of s_res to HBM.
+template <typename T, int FN>
+constexpr int smem_bytes() { return (4 + (FN == FN_IK ? 2 : 1)) * TILE * int(sizeof(T)) + TILE * 2; }
+
 template <typename T, int FN, bool TMA>
 __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : B200_MINB_K)
-    bessel_eval_kernel(const T *__restrict__ vin, const T *__restrict__ xin, T *__restrict__ out, int64_t n) {
-    __shared__ alignas(128) T s_stage[2][2][TILE];   // [buffer][v|x][element]
-    __shared__ alignas(128) T s_res[TILE];
-    __shared__ uint16_t s_idx[TILE];
+    bessel_eval_kernel(const T *__restrict__ vin, const T *__restrict__ xin, T *__restrict__ out,
+                       T *__restrict__ out2, int64_t n) {
+    constexpr int NOUT = FN == FN_IK ? 2 : 1;         // results per element (out, out2)
+    // dynamic shared memory (smem_bytes<T, FN>()): stage[2][2][TILE], res[NOUT][TILE], idx[TILE]
+    extern __shared__ __align__(128) unsigned char s_dyn[];
+    auto s_stage = reinterpret_cast<T (*)[2][TILE]>(s_dyn);                       // [buffer][v|x][element]
+    auto s_res = reinterpret_cast<T (*)[TILE]>(s_dyn + 4 * TILE * sizeof(T));     // [output][element]
+    uint16_t *s_idx = reinterpret_cast<uint16_t *>(s_dyn + (4 + NOUT) * TILE * sizeof(T));
     __shared__ uint64_t s_wtot[TPB / 32];             // per-warp bin totals, 8-bit fields
     __shared__ alignas(8) uint64_t s_bar[2];
 
@@ -344,7 +374,7 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : B200_MINB_K)
             }
         }
         if constexpr (TMA) {
-            if (tid == 0) bulk_wait_read();    // the previous tile's store has read s_res
+            if (tid == 0) bulk_wait_read();    // the previous tile's stores have read s_res
         }
         __syncthreads();
         // 3. evaluate: sorted slot p -> element j of the stage
@@ -354,7 +384,11 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : B200_MINB_K)
             if (p < rem) {
                 const int w = s_idx[p];
                 const int j = w & 0xFFF;
-                s_res[j] = eval_bin<T, FN>(w >> 12, sv[j], sx[j]);
+                if constexpr (FN == FN_IK) {
+                    eval_bin_ik<T>(w >> 12, sv[j], sx[j], s_res[0][j], s_res[NOUT - 1][j]);
+                } else {
+                    s_res[0][j] = eval_bin<T, FN>(w >> 12, sv[j], sx[j]);
+                }
             }
         }
         __syncthreads();
@@ -363,14 +397,21 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : B200_MINB_K)
             const int ra = rem & ~(VEC - 1);
             if (tid == 0 && ra > 0) {
                 fence_proxy_async();
-                bulk_store(out + base, s_res, uint32_t(ra * sizeof(T)));
+                bulk_store(out + base, s_res[0], uint32_t(ra * sizeof(T)));
+                if (NOUT == 2) bulk_store(out2 + base, s_res[NOUT - 1], uint32_t(ra * sizeof(T)));
             }
-            if (ra != rem && tid < rem - ra) out[base + ra + tid] = s_res[ra + tid];
+            if (ra != rem && tid < rem - ra) {
+                out[base + ra + tid] = s_res[0][ra + tid];
+                if (NOUT == 2) out2[base + ra + tid] = s_res[NOUT - 1][ra + tid];
+            }
         } else {
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
                 const int j = tid + i * TPB;
-                if (j < rem) __stcs(out + base + j, s_res[j]);
+                if (j < rem) {
+                    __stcs(out + base + j, s_res[0][j]);
+                    if (NOUT == 2) __stcs(out2 + base + j, s_res[NOUT - 1][j]);
+                }
             }
         }
     }
@@ -401,27 +442,30 @@ static int device_sms() {
 }
 
 template <typename T, int FN>
-static int launch_eval(const T *v, const T *x, T *out, int64_t n, cudaStream_t s) {
+static int launch_eval(const T *v, const T *x, T *out, int64_t n, cudaStream_t s, T *out2 = nullptr) {
     if (n < 0) return set_err(B200_ERR_INVALID_ARGUMENT, "n < 0");
     if (n == 0) return B200_OK;
-    if (!v || !x || !out) return set_err(B200_ERR_INVALID_ARGUMENT, "null pointer");
+    if (!v || !x || !out || (FN == FN_IK && !out2)) return set_err(B200_ERR_INVALID_ARGUMENT, "null pointer");
     // bulk copies need 16-byte aligned global addresses
     const bool tma = ((reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(x) |
-                       reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+                       reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(out2)) & 15) == 0;
+    constexpr int SMEM = smem_bytes<T, FN>();
     static int occ[2] = {0, 0};
     if (occ[tma] == 0) {
+        auto kern = tma ? bessel_eval_kernel<T, FN, true> : bessel_eval_kernel<T, FN, false>;
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+        if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute");
         int o = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-            &o, tma ? bessel_eval_kernel<T, FN, true> : bessel_eval_kernel<T, FN, false>, TPB, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, TPB, SMEM);
         occ[tma] = o > 0 ? o : 1;
     }
     const int64_t ntiles = (n + TILE - 1) / TILE;
     const int64_t resident = int64_t(device_sms()) * occ[tma];
     const int grid = int(ntiles < resident ? ntiles : resident);
     if (tma)
-        bessel_eval_kernel<T, FN, true><<<grid, TPB, 0, s>>>(v, x, out, n);
+        bessel_eval_kernel<T, FN, true><<<grid, TPB, SMEM, s>>>(v, x, out, out2, n);
     else
-        bessel_eval_kernel<T, FN, false><<<grid, TPB, 0, s>>>(v, x, out, n);
+        bessel_eval_kernel<T, FN, false><<<grid, TPB, SMEM, s>>>(v, x, out, out2, n);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     return cuda_err(cudaGetLastError(), "bessel_eval_kernel launch");
 }
@@ -436,15 +480,15 @@ struct HostPipe {
     std::mutex mu;
     int dev = -1;
     cudaStream_t st[NSLOT] = {};
-    void *buf[NSLOT] = {};   // 3 arrays of CH doubles per slot
+    void *buf[NSLOT] = {};   // 4 arrays of CH doubles per slot: v, x, out, out2
 };
 static HostPipe g_pipe;
 
 template <int FN>
-static int host_eval_f64(const double *v_h, const double *x_h, double *out_h, int64_t n) {
+static int host_eval_f64(const double *v_h, const double *x_h, double *out_h, int64_t n, double *out2_h = nullptr) {
     if (n < 0) return set_err(B200_ERR_INVALID_ARGUMENT, "n < 0");
     if (n == 0) return B200_OK;
-    if (!v_h || !x_h || !out_h) return set_err(B200_ERR_INVALID_ARGUMENT, "null pointer");
+    if (!v_h || !x_h || !out_h || (FN == FN_IK && !out2_h)) return set_err(B200_ERR_INVALID_ARGUMENT, "null pointer");
     std::lock_guard<std::mutex> lk(g_pipe.mu);
     int dev = 0;
     int rc = cuda_err(cudaGetDevice(&dev), "cudaGetDevice");
@@ -458,7 +502,7 @@ static int host_eval_f64(const double *v_h, const double *x_h, double *out_h, in
         }
         for (int i = 0; i < HostPipe::NSLOT; ++i) {
             if ((rc = cuda_err(cudaStreamCreateWithFlags(&g_pipe.st[i], cudaStreamNonBlocking), "stream"))) return rc;
-            if ((rc = cuda_err(cudaMalloc(&g_pipe.buf[i], 3 * HostPipe::CH * sizeof(double)), "cudaMalloc"))) return rc;
+            if ((rc = cuda_err(cudaMalloc(&g_pipe.buf[i], 4 * HostPipe::CH * sizeof(double)), "cudaMalloc"))) return rc;
         }
         g_pipe.dev = dev;
     }
@@ -469,13 +513,17 @@ static int host_eval_f64(const double *v_h, const double *x_h, double *out_h, in
         double *dv = static_cast<double *>(g_pipe.buf[slot]);
         double *dx = dv + HostPipe::CH;
         double *dout = dx + HostPipe::CH;
+        double *dout2 = dout + HostPipe::CH;
         cudaStream_t s = g_pipe.st[slot];
         if ((rc = cuda_err(cudaMemcpyAsync(dv, v_h + off, m * sizeof(double), cudaMemcpyHostToDevice, s), "H2D")))
             return rc;
         if ((rc = cuda_err(cudaMemcpyAsync(dx, x_h + off, m * sizeof(double), cudaMemcpyHostToDevice, s), "H2D")))
             return rc;
-        if ((rc = launch_eval<double, FN>(dv, dx, dout, m, s))) return rc;
+        if ((rc = launch_eval<double, FN>(dv, dx, dout, m, s, dout2))) return rc;
         if ((rc = cuda_err(cudaMemcpyAsync(out_h + off, dout, m * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H")))
+            return rc;
+        if (FN == FN_IK &&
+            (rc = cuda_err(cudaMemcpyAsync(out2_h + off, dout2, m * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H")))
             return rc;
     }
     for (int i = 0; i < HostPipe::NSLOT; ++i)
@@ -502,6 +550,12 @@ int b200_log_kv_f64(const double *v, const double *x, double *out, int64_t n, vo
 int b200_log_kv_f32(const float *v, const float *x, float *out, int64_t n, void *stream) {
     return launch_eval<float, FN_K>(v, x, out, n, static_cast<cudaStream_t>(stream));
 }
+int b200_log_ivkv_f64(const double *v, const double *x, double *out_i, double *out_k, int64_t n, void *stream) {
+    return launch_eval<double, FN_IK>(v, x, out_i, n, static_cast<cudaStream_t>(stream), out_k);
+}
+int b200_log_ivkv_f32(const float *v, const float *x, float *out_i, float *out_k, int64_t n, void *stream) {
+    return launch_eval<float, FN_IK>(v, x, out_i, n, static_cast<cudaStream_t>(stream), out_k);
+}
 int b200_log_kv_paper_f64(const double *v, const double *x, double *out, int64_t n, void *stream) {
     return launch_eval<double, FN_K_PAPER>(v, x, out, n, static_cast<cudaStream_t>(stream));
 }
@@ -522,6 +576,9 @@ int b200_log_iv_f64_host(const double *v_h, const double *x_h, double *out_h, in
 }
 int b200_log_kv_f64_host(const double *v_h, const double *x_h, double *out_h, int64_t n) {
     return host_eval_f64<FN_K>(v_h, x_h, out_h, n);
+}
+int b200_log_ivkv_f64_host(const double *v_h, const double *x_h, double *out_i_h, double *out_k_h, int64_t n) {
+    return host_eval_f64<FN_IK>(v_h, x_h, out_i_h, n, out_k_h);
 }
 
 const char *b200_last_error(void) { return g_err; }

@@ -245,6 +245,61 @@ __device__ __forceinline__ T log_bessel_u(T v, T x) {
     return IS_K ? tail - veta : veta + tail;
 }
 
+// ---------------------------------------------------------------- fused I + K
+// Both functions at the same (v, x) share everything but the sign pattern of
+// the expansion: with w = t/v, Eq. (log Iv u k) sums u_k(t) w^k and Eq. (log Kv
+// u k) sums (-1)^k u_k(t) w^k, so with the even / odd parts E, O of the sum
+// S_I = 1 + E + O and S_K = 1 + E - O; likewise the mu expansions differ only
+// by (-1)^k.  One rsqrt, one Horner pass per P_k, one v*eta (its log) serve
+// both results; only the final log per function is separate.
+template <typename T, int KU>
+__device__ __forceinline__ void log_bessel_u_ik(T v, T x, T &li, T &lk) {
+    const T rho2 = fma(v, v, x * x);
+    const T y = fm_rsqrt(rho2);                  // 1 / rho = t / v
+    const T rho = rho2 * y;
+    const T t = v * y;
+    const T t2 = t * t, w2 = y * y;
+    // E = sum_{k even >= 2} P_k w^k, O = sum_{k odd} P_k w^k (Horner in w^2)
+    constexpr int KE = (KU / 2) * 2, KO = KU - ((KU + 1) % 2);
+    T e = uk_row<T>(KE, t2);
+#pragma unroll
+    for (int k = KE - 2; k >= 2; k -= 2) e = fma(e, w2, uk_row<T>(k, t2));
+    e *= w2;
+    T o = uk_row<T>(KO, t2);
+#pragma unroll
+    for (int k = KO - 2; k >= 1; k -= 2) o = fma(o, w2, uk_row<T>(k, t2));
+    o *= y;
+    const T SI = T(1) + e + o, SK = T(1) + e - o;
+    const T veta = v_times_eta<T, false>(v, x, v, x, rho, rho);
+    li = veta + T(0.5) * fm_log(SI * SI * y * T(0.5 / CUDART_PI));
+    lk = T(0.5) * fm_log(SK * SK * y * T(CUDART_PI / 2.0)) - veta;
+}
+
+template <typename T>
+__device__ __forceinline__ void log_bessel_mu_ik(T v, T x, T &li, T &lk) {
+    const T rx = fm_rcp(x);
+    const T mu = T(4) * v * v;
+    const T c = T(0.125) * rx;
+    T term = T(1), si = T(1), sk = T(1);          // K terms (all signs +); I alternates
+    // terms in (odd, even) pairs, fully unrolled: (2k-1)^2 and 1/k are constants
+#pragma unroll
+    for (int k = 1; k < KMU; k += 2) {
+        T i1, i2;
+        if constexpr (sizeof(T) == 8) { i1 = c_inv_d[k]; i2 = c_inv_d[k + 1]; }
+        else { i1 = T(1.0 / k); i2 = T(1.0 / (k + 1)); }
+        term *= (mu - T((2 * k - 1) * (2 * k - 1))) * (c * i1);
+        si -= term;                                // summed in order, as the separate
+        sk += term;                                // series (no even/odd cancellation)
+        term *= (mu - T((2 * k + 1) * (2 * k + 1))) * (c * i2);
+        si += term;
+        sk += term;
+        if (k >= 3 && fabs(term) <= Tr<T>::eps * T(0.25) * fabs(si)) break;
+    }
+    const T SI = fabs(si), SK = fabs(sk);
+    li = x + T(0.5) * fm_log(SI * SI * rx * T(0.5 / CUDART_PI));
+    lk = -x + T(0.5) * fm_log(SK * SK * rx * T(CUDART_PI / 2.0));
+}
+
 // ---------------------------------------------------------------- series (I)
 // Eq. (Iv infinite series) (line 127) with the recurrence Eqs. (ak recurrence
 // base)/(ak recurrence) (lines 148-150) and the logarithm-of-a-sum form

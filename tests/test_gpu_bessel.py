@@ -241,3 +241,59 @@ def test_stability_sweep(B, fn):
     vs, xs, gs = map(np.concatenate, (samples_v, samples_x, samples_g))
     e = oracle.rel_err(gs, _ref(fn, vs, xs))
     assert e.max() <= TOL64, e.max()
+
+
+# ------------------------------------------------------------------ fused I + K
+def _run_ivkv(B, v, x, dtype=torch.float64):
+    oi, ok = B.log_ivkv(_dev(v, dtype), _dev(x, dtype))
+    torch.cuda.synchronize()
+    return oi.double().cpu().numpy(), ok.double().cpu().numpy()
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("case", ["config0", "ragged", "wide", "eta", "special"])
+def test_fused_ivkv_against_oracle(B, case):
+    """b200_log_ivkv_f64: both functions in one pass, each within the f64 bar."""
+    if case == "config0":
+        v, x = workloads.small_case(10_000, seed=30)
+    elif case == "ragged":
+        rng = np.random.default_rng(31)
+        v = np.exp(rng.uniform(math.log(1e-3), math.log(2e3), 4097))
+        x = np.exp(rng.uniform(math.log(1e-3), math.log(2e3), 4097))
+    elif case == "wide":
+        v = workloads.log_uniform(30_000, 1e-3, 1e5, seed=32)
+        x = workloads.log_uniform(30_000, 1e-3, 1e5, seed=33)
+    elif case == "eta":
+        v = workloads.log_uniform(10_000, 50.0, 1e5, seed=34)
+        x = v * 0.66274341934918158 * (1 + np.random.default_rng(35).uniform(-0.1, 0.1, v.size))
+    else:
+        v = np.array([0.0, 3.0, 0.0, 2.0, -1.0, 1.0, 1.0, 20.0, 0.5, 1e150, 5.0])
+        x = np.array([0.0, 0.0, 1e-300, -1.0, 2.0, np.nan, np.inf, 0.0, 1e300, 3.0, 1e-200])
+    gi, gk = _run_ivkv(B, v, x)
+    si = _run(B, "iv", v, x)
+    sk = _run(B, "kv", v, x)
+    # same special values / NaN pattern as the separate calls
+    assert np.array_equal(np.isnan(gi), np.isnan(si)) and np.array_equal(np.isnan(gk), np.isnan(sk))
+    assert np.array_equal(np.isinf(gi), np.isinf(si)) and np.array_equal(np.isinf(gk), np.isinf(sk))
+    if case == "special":      # extreme arguments: agree with the separate calls (no oracle run)
+        ok = np.isfinite(si) & np.isfinite(sk)
+        assert oracle.rel_err(gi[ok], si[ok]).max() <= TOL64 and oracle.rel_err(gk[ok], sk[ok]).max() <= TOL64
+        return
+    ok = np.isfinite(si) & np.isfinite(sk)
+    ri = oracle.log_iv(np.abs(v[ok]), x[ok])
+    rk = oracle.log_kv(v[ok], x[ok])
+    assert oracle.rel_err(gi[ok], ri).max() <= TOL64
+    assert oracle.rel_err(gk[ok], rk).max() <= TOL64
+
+
+def test_fused_ivkv_f32_and_host(B):
+    v, x = workloads.small_case(10_000, seed=36)
+    gi, gk = _run_ivkv(B, v, x, torch.float32)
+    v32 = np.asarray(v, np.float32).astype(np.float64)
+    x32 = np.asarray(x, np.float32).astype(np.float64)
+    assert oracle.rel_err(gi, oracle.log_iv(v32, x32)).max() <= TOL32
+    assert oracle.rel_err(gk, oracle.log_kv(v32, x32)).max() <= TOL32
+    v, x = workloads.bench_grid_numpy(30_000, seed=37)
+    hi, hk = B.log_ivkv_host(v, x)
+    di, dk = _run_ivkv(B, v, x)
+    assert np.array_equal(hi, di) and np.array_equal(hk, dk)

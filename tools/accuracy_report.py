@@ -34,9 +34,15 @@ def main(n=20000, seed=0):
             e = oracle.rel_err(got, ref)
             i = int(np.argmax(e))
             row[fn] = {"max": float(e[i]), "p99": float(np.quantile(e, 0.99)), "at": [float(v[i]), float(x[i])]}
+        fi, fk = B.log_ivkv(vt, xt)
+        for nm, got, ref in (("ivkv_i", fi, oracle.log_iv(v, x)), ("ivkv_k", fk, oracle.log_kv(v, x))):
+            e = oracle.rel_err(got.cpu().numpy(), ref)
+            i = int(np.argmax(e))
+            row[nm] = {"max": float(e[i]), "p99": float(np.quantile(e, 0.99)), "at": [float(v[i]), float(x[i])]}
         res[name] = row
         print(f"{name:10s} I max {row['iv']['max']:.2e} p99 {row['iv']['p99']:.1e} at {row['iv']['at']}   "
-              f"K max {row['kv']['max']:.2e} p99 {row['kv']['p99']:.1e} at {row['kv']['at']}", flush=True)
+              f"K max {row['kv']['max']:.2e} p99 {row['kv']['p99']:.1e} at {row['kv']['at']}   "
+              f"fused I {row['ivkv_i']['max']:.2e} K {row['ivkv_k']['max']:.2e} at {row['ivkv_k']['at']}", flush=True)
     return res
 
 

@@ -27,7 +27,7 @@ for w in $WHAT; do
     methods)
       timeout 600 python tools/method_bench.py > $OUT/methods.json 2> $OUT/methods.err ;;
     full)
-      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:bessel_eval_kernel -s 2 -c 2 \
+      timeout 1500 ncu --set full --clock-control none --import-source on -k regex:bessel_eval_kernel -s 1 -c 3 \
         -o $OUT/prof -f python bench.py --steps 1 --warmup 1 --skip-e2e --skip-cpu-baseline --n-per-v 2000000 > $OUT/ncu_full.log 2>&1 ;;
   esac
 done

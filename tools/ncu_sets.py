@@ -17,7 +17,7 @@ SETS = [
 ]
 
 
-def run(n=4_000_000):
+def run(n=4_000_000, fused=False):
     import torch
     sys.path.insert(0, ".")
     import paper_2409_08729_b200 as B
@@ -26,16 +26,19 @@ def run(n=4_000_000):
     for name, (v0, v1), (x0, x1) in SETS:
         v = torch.empty(n, dtype=torch.float64, device=dev).uniform_(v0, v1, generator=g)
         x = torch.empty(n, dtype=torch.float64, device=dev).uniform_(x0, x1, generator=g)
-        B.log_iv(v, x)
-        B.log_kv(v, x)
+        if fused:
+            B.log_ivkv(v, x)
+        else:
+            B.log_iv(v, x)
+            B.log_kv(v, x)
     torch.cuda.synchronize()
 
 
-def parse(rep, n=4_000_000):
+def parse(rep, n=4_000_000, fused=False):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
     h = rows[0]
-    names = [f"{s[0]}/{fn}" for s in SETS for fn in ("I", "K")]
+    names = [f"{s[0]}/{fn}" for s in SETS for fn in (("IK",) if fused else ("I", "K"))]
     res = {}
     for i, r in enumerate(rows[2:]):
         d = dict(zip(h, r))
@@ -67,7 +70,11 @@ def parse(rep, n=4_000_000):
 
 
 if __name__ == "__main__":
-    if len(sys.argv) > 1 and sys.argv[1] == "parse":
-        json.dump(parse(sys.argv[2]), open(sys.argv[3], "w"), indent=1) if len(sys.argv) > 3 else parse(sys.argv[2])
+    fz = "--fused" in sys.argv
+    args = [a for a in sys.argv[1:] if a != "--fused"]
+    if args and args[0] == "parse":
+        r = parse(args[1], fused=fz)
+        if len(args) > 2:
+            json.dump(r, open(args[2], "w"), indent=1)
     else:
-        run()
+        run(fused=fz)

@@ -122,9 +122,10 @@ def main():
         counts = {}
         for e in json.load(open(os.path.join(dst, "ncu_full.json"))):
             m = re.search(r"bessel_eval_kernel<double, (?:\(int\))?(\d)[,>]", e["kernel"])
-            fn = {"0": "log_iv", "1": "log_kv"}.get(m.group(1)) if m else None
+            fn = {"0": "log_iv", "1": "log_kv", "3": "log_ivkv"}.get(m.group(1)) if m else None
             if fn and "double" in e["kernel"] and "bessel_eval_kernel" in e["kernel"] and e.get("fp64_flop_per_eval"):
                 counts[fn] = {"fp64_flop_per_eval": e["fp64_flop_per_eval"],
+                              "per": "pair (log I and log K)" if fn == "log_ivkv" else "evaluation",
                               "dram_bytes_per_eval": e.get("dram_bytes_per_eval"),
                               "source": f"profiles/{tag}/ncu_full.json ({e['pairs']} pairs, bench grid)"}
         json.dump(counts, open(os.path.join(ROOT, "profiles", "roofline_counts.json"), "w"), indent=1)

@@ -47,6 +47,9 @@ def run(names, n=20_000_000, reps=5):
         for f in ("b200_log_iv_f64", "b200_log_kv_f64"):
             getattr(L, f).argtypes = [ctypes.c_void_p] * 3 + [ctypes.c_int64, ctypes.c_void_p]
             getattr(L, f).restype = ctypes.c_int
+        if hasattr(L, "b200_log_ivkv_f64"):
+            L.b200_log_ivkv_f64.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_void_p]
+            L.b200_log_ivkv_f64.restype = ctypes.c_int
         libs[nm] = L
     g = torch.Generator(device=dev).manual_seed(0)
     sets = {}
@@ -90,10 +93,22 @@ def run(names, n=20_000_000, reps=5):
                 torch.cuda.synchronize()
                 ms = e0.elapsed_time(e1) / reps
                 row[fn] = {"ms": round(ms, 4), "gevals": round(n / ms / 1e6, 2), "maxdiff": dev_}
+            if hasattr(L, "b200_log_ivkv_f64"):
+                o1, o2 = torch.empty_like(v), torch.empty_like(v)
+                L.b200_log_ivkv_f64(v.data_ptr(), xx.data_ptr(), o1.data_ptr(), o2.data_ptr(), n, s)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(reps):
+                    L.b200_log_ivkv_f64(v.data_ptr(), xx.data_ptr(), o1.data_ptr(), o2.data_ptr(), n, s)
+                e1.record()
+                torch.cuda.synchronize()
+                row["ivkv"] = {"ms": round(e0.elapsed_time(e1) / reps, 4),
+                               "maxdiff": max(float(((o1 - ref["log_iv"]).abs() / ref["log_iv"].abs().clamp_min(1.0)).max()),
+                                              float(((o2 - ref["log_kv"]).abs() / ref["log_kv"].abs().clamp_min(1.0)).max()))}
             res.setdefault(sname, {})[nm] = row
     # bench-grid totals (sum over the 11 order slices)
     tot = {nm: {fn: round(sum(res[f"v={2 ** j}"][nm][fn]["ms"] for j in range(11)), 3)
-                for fn in ("log_iv", "log_kv")} for nm in names}
+                for fn in ("log_iv", "log_kv", "ivkv") if fn in res["v=1"][nm]} for nm in names}
     print(json.dumps({"sets": res, "bench_grid_ms": tot}, indent=1))
 
 
