@@ -324,22 +324,37 @@ __device__ __forceinline__ T log_iv_series(T v, T x) {
     if (x == T(0)) return v == T(0) ? T(0) : T(-CUDART_INF);
     if constexpr (sizeof(T) == 8) {
         const T q = T(0.25) * x * x;
-        T N = T(1), P = T(1), Q = T(1), vk = v;
+        T N = T(1), P = T(1), Q = T(1), vk = v, kd = T(0);
         for (int k = 1; k < 400; k += 2) {
             vk += T(1);
-            const T d0 = T(k) * vk;
+            kd += T(1);
+            const T d0 = kd * vk;
             Q *= q;
             N = fma(N, d0, Q);
             P *= d0;
             vk += T(1);
-            const T d1 = T(k + 1) * vk;
+            kd += T(1);
+            const T d1 = kd * vk;
             Q *= q;
             N = fma(N, d1, Q);
             P *= d1;
             if (Q <= N * Tr<T>::eps) break;
         }
+        // a_0 = 1/Gamma(v+1) = rg(mu) / prod_{j=1..n} (mu + j), v = n + mu, |mu| <= 1/2,
+        // rg(z) = 1/Gamma(1+z) by its Taylor series (tables.h) -- no lgamma call
+        const T fl = floor(v + T(0.5));
+        const T mu = v - fl;
+        const int nl = int(fl);
+        T pr = T(1), m = mu;
+        for (int j = 0; j < nl; ++j) {
+            m += T(1);
+            pr *= m;
+        }
+        T g = T(c_rg_d[B200_RGAMMA_NT - 1]);
+#pragma unroll
+        for (int j = B200_RGAMMA_NT - 2; j >= 0; --j) g = fma(g, mu, T(c_rg_d[j]));
         const T lx = SAFE ? fm_log_wide(T(0.5) * x) : fm_log(T(0.5) * x);
-        return fma(v, lx, fm_log(fm_div(N, P)) - d_lgamma(v + T(1)));
+        return fma(v, lx, fm_log(fm_div(N * g, P * pr)));
     }
     const T q = T(0.25) * x * x;
     T b = T(1), S = T(1);
