@@ -34,6 +34,9 @@ namespace b200 {
 #ifndef B200_MINB_K
 #define B200_MINB_K 4        // CTAs per SM for log K
 #endif
+#ifndef B200_MINB_IK
+#define B200_MINB_IK 4       // CTAs per SM for the fused I + K pass
+#endif
 #ifndef B200_ITEMS
 #define B200_ITEMS 4
 #endif
@@ -239,7 +242,7 @@ template <typename T, int FN>
 constexpr int smem_bytes() { return (4 + (FN == FN_IK ? 2 : 1)) * TILE * int(sizeof(T)) + TILE * 2; }
 
 template <typename T, int FN, bool TMA>
-__global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : B200_MINB_K)
+__global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B200_MINB_IK : B200_MINB_K)
     bessel_eval_kernel(const T *__restrict__ vin, const T *__restrict__ xin, T *__restrict__ out,
                        T *__restrict__ out2, int64_t n) {
     constexpr int NOUT = FN == FN_IK ? 2 : 1;         // results per element (out, out2)

@@ -451,8 +451,9 @@ __device__ __forceinline__ T temme_kmu(T mu, T x, T &rho) {
 // t_k = k h the nodes are
 //   K_nu = (h/2) e^{-x} [1 + sum_{k>=1} e^{-2x sinh^2(t_k/2)} (E_nu^k + E_nu^{-k})],  E_nu = e^{nu h},
 // sinh(t_k/2) by the three-term recurrence s_{k+1} = 2 cosh(h/2) s_k - s_{k-1}
-// (sinh grows, so the recurrence is stable), one exp per node shared by both
-// orders, all terms positive.  The integrand is unimodal in t and its first
+// and 2 cosh(k nu h) by C_{k+1} = 2 cosh(nu h) C_k - C_{k-1} (growing solutions
+// dominate: forward-stable), one exp per node shared by both orders, all terms
+// positive.  The integrand is unimodal in t and its first
 // node is already O(1) of the k = 0 term (2x sinh^2(h/2) < 0.4), so a term
 // below eps of the sum only occurs past the peak: stop at the first K_{mu+1}
 // term (the wider integrand) below eps of its sum.
@@ -464,23 +465,28 @@ __device__ __forceinline__ T trap_kmu(T mu, T x, T &rho) {
     // sinh(a) and 2 cosh(a) by their Taylor series (a <= 0.12: 5 terms exact to 2^-60)
     const T s1 = a * fma(a2 * T(1.0 / 6), fma(a2 * T(1.0 / 20), fma(a2 * T(1.0 / 42), fma(a2, T(1.0 / 72), T(1)), T(1)), T(1)), T(1));
     const T c = fma(a2, fma(a2 * T(1.0 / 12), fma(a2 * T(1.0 / 30), fma(a2, T(1.0 / 56), T(1)), T(1)), T(1)), T(2));
+    // 2 cosh(k nu h) for nu = mu, mu+1 by the recurrence C_{k+1} = c C_k - C_{k-1},
+    // c = 2 cosh(nu h) (forward-stable: the growing solution dominates)
     const T Em = fm_exp(mu * h), Emi = fm_rcp(Em);
-    const T eh = fm_exp(h), ehi = fm_rcp(eh);
-    const T Ep = Em * eh, Epi = Emi * ehi;
-    T pm = T(1), pmi = T(1), pp = T(1), ppi = T(1);
+    const T eh = fm_exp(h);
+    const T cm = Em + Emi, cp = fma(Em, eh, Emi * fm_rcp(eh));
+    T ap = T(2), ac = cm, bp = T(2), bc = cp;          // C_{k-1}, C_k (orders mu, mu+1), k = 1
     T A = T(1), B = T(1), sp = T(0), sk = s1;
     const T m2x = T(-2) * x;
-    for (int k = 1; k < 64; k += 2) {     // two nodes per trip, stop test on the second
+    for (int k = 1; k < 64; k += 2) {     // nodes k, k+1 per trip, stop test on the second
         const T s2 = fma(c, sk, -sp);
         const T e1 = fm_exp_nc(m2x * sk * sk), e2 = fm_exp_nc(m2x * s2 * s2);
-        pm *= Em; pmi *= Emi; pp *= Ep; ppi *= Epi;
-        A = fma(e1, pm + pmi, A);
-        B = fma(e1, pp + ppi, B);
-        pm *= Em; pmi *= Emi; pp *= Ep; ppi *= Epi;
-        const T tb = e2 * (pp + ppi);
-        A = fma(e2, pm + pmi, A);
+        const T an = fma(cm, ac, -ap), bn = fma(cp, bc, -bp);          // C_{k+1}
+        A = fma(e1, ac, A);
+        B = fma(e1, bc, B);
+        const T tb = e2 * bn;
+        A = fma(e2, an, A);
         B += tb;
         if (tb <= B * Tr<T>::eps) break;
+        ap = an;                                                        // C_{k+1}
+        ac = fma(cm, an, -ac);                                          // C_{k+2}
+        bp = bn;
+        bc = fma(cp, bn, -bc);
         sp = s2;
         sk = fma(c, s2, -sk);
     }
