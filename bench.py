@@ -202,6 +202,59 @@ def _timed(step, steps, stream, dist):
     return ms
 
 
+def run_extra(args, B, workloads, ws, rank, dev, stream, dist):
+    """Secondary measurements on the other BASELINE configs (not the headline):
+    configs[3] stability sweep (rows sharded over the ranks, strong scaling) and
+    configs[4] vMF fit on 50000 x d unit-norm features (rows sharded, one
+    all-reduce of the d-vector)."""
+    import torch
+    from paper_2409_08729_b200.parallel import shard_range
+    out = {}
+    # -- configs[3]: v in {0} U logspace(1e-3,1e5) x x in logspace(1e-3,1e5), 16384^2 pairs
+    nv = nx = 16384
+    r0, r1 = shard_range(nv, ws, rank)
+    sv, sx = workloads.stability_grid(nv, nx, device=dev, rows=(r0, r1))
+    oi, ok = torch.empty_like(sv), torch.empty_like(sv)
+    B.log_ivkv(sv, sx, oi, ok)
+    torch.cuda.synchronize()
+    bad = int((~torch.isfinite(oi)).sum().item() + (~torch.isfinite(ok)).sum().item())
+    if dist:
+        t = torch.tensor([bad], dtype=torch.float64, device=dev)
+        dist.all_reduce(t)
+        bad = int(t.item())
+    reps = 3
+    ms = _timed(lambda: B.log_ivkv(sv, sx, oi, ok), reps, stream, dist)
+    out["stability_sweep"] = {
+        "config": "BASELINE configs[3]: v in {0} U logspace(1e-3,1e5) x x in logspace(1e-3,1e5), "
+                  f"{nv}x{nx} = {nv * nx} pairs, rows sharded over {ws} GPU(s), fused log I + log K",
+        "value": 2 * nv * nx * reps / (ms / 1e3) / 1e9, "unit": UNIT, "ms_per_pass": ms / reps,
+        "nonfinite_outputs": bad, "scaling": "strong"}
+    del sv, sx, oi, ok
+    # -- configs[4]: vMF MLE on 50000 x d features (f32), rows sharded
+    n = 50_000
+    lo, hi = shard_range(n, ws, rank)
+    hbm_peak, _ = _peaks()
+    vm = {}
+    for d in (2048, 8192, 32768):
+        X, _ = workloads.vmf_features(hi - lo, d, rbar=0.15, seed=100 + rank, device=dev)
+        pg = dist.group.WORLD if dist else None
+        mu, st = B.vmf_fit(X, process_group=pg)
+        torch.cuda.synchronize()
+        reps = 5
+        ms = _timed(lambda: B.vmf_fit(X, process_group=pg), reps, stream, dist)
+        cs = torch.empty(d, dtype=torch.float64, device=dev)
+        ms_cs = _timed(lambda: B.vmf_colsum(X, out=cs), reps, stream, None)
+        gbs = (hi - lo) * d * 4 / (ms_cs / reps / 1e3) / 1e9
+        vm[str(d)] = {"ms_per_fit": ms / reps, "colsum_ms": ms_cs / reps,
+                      "colsum_roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+                                          "frac": gbs / hbm_peak},
+                      "rbar": float(st[0].item()), "kappa_mle": float(st[4].item())}
+        del X
+    out["vmf_fit"] = {"config": f"BASELINE configs[4]: {n} x d unit-norm f32 features (Rbar 0.15), rows sharded "
+                                f"over {ws} GPU(s), one all-reduce of the d-vector", "per_d": vm}
+    return out
+
+
 def run_ours(args):
     import torch
 
@@ -226,12 +279,13 @@ def run_ours(args):
     def step():
         B.log_ivkv(v, x, out_i, out_k)
 
+    # clock sampler from the warm-up through the timed region (NVML needs a few ms to start)
+    clocks = Clocks(lrank) if rank == 0 else None
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     # non-finite guard on the warm-up outputs (the method never produces inf/NaN here)
     nonfinite = int((~torch.isfinite(out_i)).sum().item() + (~torch.isfinite(out_k)).sum().item())
-    clocks = Clocks(lrank) if rank == 0 else None
     launches0 = B.launch_count()
     ms = _timed(step, args.steps, stream, dist)
     launches = B.launch_count() - launches0
@@ -291,6 +345,8 @@ def run_ours(args):
                        "both results come back; chunked H2D/kernel/D2H pipeline on 3 streams; host wall clock"}
         del vh, xh, oi, ok
 
+    extra = None if args.skip_extra else run_extra(args, B, workloads, ws, rank, dev, stream, dist)
+    del v, x, out_i, out_k
     if rank != 0:
         return
     hbm_peak, hbm_src = _peaks()
@@ -330,6 +386,7 @@ def run_ours(args):
         "gpu_launches": launches,
         "nonfinite_outputs": nonfinite,
         "separate_calls": sep,
+        "extra": extra,
         "e2e": e2e,
         "clocks": clk,
     }
@@ -347,6 +404,7 @@ def main():
     ap.add_argument("--n-per-v", type=int, default=N_PER_V)
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-separate", action="store_true")
+    ap.add_argument("--skip-extra", action="store_true")
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()

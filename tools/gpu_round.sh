@@ -23,12 +23,12 @@ for w in $WHAT; do
       timeout 900 python bench.py > $OUT/bench.json 2> $OUT/bench.err; echo "bench exit $?" >> $OUT/bench.err ;;
     launches)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $OUT/launches.csv \
-        python bench.py --steps 2 --warmup 1 --skip-e2e --skip-cpu-baseline > $OUT/launches_bench.log 2>&1 ;;
+        python bench.py --steps 2 --warmup 1 --skip-e2e --skip-cpu-baseline --skip-extra > $OUT/launches_bench.log 2>&1 ;;
     methods)
       timeout 600 python tools/method_bench.py > $OUT/methods.json 2> $OUT/methods.err ;;
     full)
       timeout 1500 ncu --set full --clock-control none --import-source on -k regex:bessel_eval_kernel -s 1 -c 3 \
-        -o $OUT/prof -f python bench.py --steps 1 --warmup 1 --skip-e2e --skip-cpu-baseline --n-per-v 2000000 > $OUT/ncu_full.log 2>&1 ;;
+        -o $OUT/prof -f python bench.py --steps 1 --warmup 1 --skip-e2e --skip-cpu-baseline --skip-extra --n-per-v 2000000 > $OUT/ncu_full.log 2>&1 ;;
   esac
 done
 ls -la $OUT
