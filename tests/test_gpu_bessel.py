@@ -297,3 +297,34 @@ def test_fused_ivkv_f32_and_host(B):
     hi, hk = B.log_ivkv_host(v, x)
     di, dk = _run_ivkv(B, v, x)
     assert np.array_equal(hi, di) and np.array_equal(hk, dk)
+
+
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_unaligned_pointers_use_the_cp_async_path(B, dtype):
+    """Views starting one element into an allocation are not 16-byte aligned: the
+    kernel falls back from bulk (TMA) copies to per-thread cp.async; same results."""
+    v, x = workloads.bench_grid_numpy(3000, seed=40)
+    vt = torch.tensor(np.concatenate([[1.0], v]), dtype=dtype, device="cuda:0")
+    xt = torch.tensor(np.concatenate([[1.0], x]), dtype=dtype, device="cuda:0")
+    va, xa = vt[1:], xt[1:]
+    assert va.data_ptr() % 16 != 0
+    outs = torch.empty(v.size + 1, dtype=dtype, device="cuda:0")[1:]
+    for fn in (B.log_iv, B.log_kv):
+        got = fn(va, xa, out=outs).clone()
+        ref = fn(va.clone(), xa.clone())
+        assert torch.equal(got, ref)
+    gi, gk = B.log_ivkv(va, xa)
+    ri, rk = B.log_ivkv(va.clone(), xa.clone())
+    assert torch.equal(gi, ri) and torch.equal(gk, rk)
+    if dtype == torch.float64:
+        e = oracle.rel_err(gi.cpu().numpy(), oracle.log_iv(v, x))
+        assert e.max() <= TOL64
+
+
+def test_tile_tails_against_separate_sizes(B):
+    """Every tail length of the last tile (bulk part + < 2 leftover elements)."""
+    v, x = workloads.bench_grid_numpy(400, seed=41)
+    full_i = _run(B, "iv", v, x)
+    for n in (1, 2, 3, 1023, 1025, 2047, 2049, 3001):
+        got = _run(B, "iv", v[:n], x[:n])
+        assert np.array_equal(got, full_i[:n]), n
