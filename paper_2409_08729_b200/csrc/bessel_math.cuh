@@ -143,6 +143,22 @@ __device__ __forceinline__ T log_bessel_mu(T v, T x) {
     return (IS_K ? -x : x) + log(S) - T(0.5) * (l2 + log(x));
 }
 
+// log(1 + d) for the U-expansion sums S = 1 + d: |d| <= sum_k M_k / rho^k with
+// rho = sqrt(v^2 + x^2), i.e. |d| < 0.0105 in the U13 region (rho >= 12.69),
+// 1.6e-3 for U9 (rho >= 80), 4.5e-4 for U6, 7e-5 for U4 (R12 bounds).  The
+// Taylor polynomial of degree NP leaves |d|^(NP+1)/(NP+1) < 2^-60: NP = 9, 6,
+// 5, 4.  Replaces a full log of S (one table log per function saved).
+template <int KU> struct Log1pDeg { static constexpr int v = KU >= 13 ? 9 : KU >= 9 ? 6 : KU >= 6 ? 5 : 4; };
+static __constant__ double c_l1p[10] = {0.0, 1.0, -1.0 / 2, 1.0 / 3, -1.0 / 4, 1.0 / 5, -1.0 / 6, 1.0 / 7,
+                                        -1.0 / 8, 1.0 / 9};
+template <typename T, int NP>
+__device__ __forceinline__ T log1p_small(T d) {
+    T p = T(c_l1p[NP]);
+#pragma unroll
+    for (int k = NP - 1; k >= 1; --k) p = fma(p, d, T(c_l1p[k]));
+    return p * d;
+}
+
 // ---------------------------------------------------------------- U_13
 // Eq. (log Iv u k) (lines 211-215) / Eq. (log Kv u k) (lines 241-245):
 //   x' = x/v, t = 1/sqrt(1+x'^2), eta = sqrt(1+x'^2) + log(x'/(1+sqrt(1+x'^2)))
@@ -237,11 +253,11 @@ __device__ __forceinline__ T log_bessel_u(T v, T x) {
     T acc = uk_row<T>(KU, t2);
 #pragma unroll
     for (int k = KU - 1; k >= 1; --k) acc = fma(acc, w, uk_row<T>(k, t2));
-    const T S = fabs(fma(acc, w, T(1)));
+    const T d = acc * w;                         // S - 1
     const T veta = v_times_eta<T, SAFE>(v, x, vs, xs, rhos, rho);
-    // 1/2 log(S^2 y_true c) with y_true = s y
+    // log S + 1/2 log(y_true c) with y_true = s y
     const T c = IS_K ? T(CUDART_PI / 2.0) : T(0.5 / CUDART_PI);
-    const T tail = T(0.5) * (fm_log(S * S * y * c) + ls);
+    const T tail = log1p_small<T, Log1pDeg<KU>::v>(d) + T(0.5) * (fm_log(y * c) + ls);
     return IS_K ? tail - veta : veta + tail;
 }
 
@@ -269,10 +285,12 @@ __device__ __forceinline__ void log_bessel_u_ik(T v, T x, T &li, T &lk) {
 #pragma unroll
     for (int k = KO - 2; k >= 1; k -= 2) o = fma(o, w2, uk_row<T>(k, t2));
     o *= y;
-    const T SI = T(1) + e + o, SK = T(1) + e - o;
     const T veta = v_times_eta<T, false>(v, x, v, x, rho, rho);
-    li = veta + T(0.5) * fm_log(SI * SI * y * T(0.5 / CUDART_PI));
-    lk = T(0.5) * fm_log(SK * SK * y * T(CUDART_PI / 2.0)) - veta;
+    // log S_I = log1p(e + o), log S_K = log1p(e - o); one log of y for both:
+    // 1/2 log(y pi/2) = 1/2 log(y/(2 pi)) + log(pi)
+    const T hl = T(0.5) * fm_log(y * T(0.5 / CUDART_PI));
+    li = veta + (hl + log1p_small<T, Log1pDeg<KU>::v>(e + o));
+    lk = (hl + T(1.1447298858494002)) + log1p_small<T, Log1pDeg<KU>::v>(e - o) - veta;
 }
 
 template <typename T>
