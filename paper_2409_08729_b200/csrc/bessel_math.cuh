@@ -343,19 +343,16 @@ __device__ __forceinline__ T log_iv_series(T v, T x) {
     if constexpr (sizeof(T) == 8) {
         const T q = T(0.25) * x * x;
         T N = T(1), P = T(1), Q = T(1), vk = v, kd = T(0);
-        for (int k = 1; k < 400; k += 2) {
-            vk += T(1);
-            kd += T(1);
-            const T d0 = kd * vk;
-            Q *= q;
-            N = fma(N, d0, Q);
-            P *= d0;
-            vk += T(1);
-            kd += T(1);
-            const T d1 = kd * vk;
-            Q *= q;
-            N = fma(N, d1, Q);
-            P *= d1;
+        for (int k = 1; k < 400; k += 4) {      // four terms per trip, one stop test
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                vk += T(1);
+                kd += T(1);
+                const T d = kd * vk;
+                Q *= q;
+                N = fma(N, d, Q);
+                P *= d;
+            }
             if (Q <= N * Tr<T>::eps) break;
         }
         // a_0 = 1/Gamma(v+1) = rg(mu) / prod_{j=1..n} (mu + j), v = n + mu, |mu| <= 1/2,
