@@ -380,7 +380,9 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
             if (tid == 0) bulk_wait_read();    // the previous tile's stores have read s_res
         }
         __syncthreads();
-        // 3. evaluate: sorted slot p -> element j of the stage
+        // 3. evaluate: sorted slot p -> element j of the stage (warp w takes the
+        //    32-slot chunks w, w + 8, w + 16, w + 24: the expensive high bins at
+        //    the end of the order land on different warps)
 #pragma unroll 1
         for (int i = 0; i < ITEMS; ++i) {
             const int p = tid + i * TPB;
