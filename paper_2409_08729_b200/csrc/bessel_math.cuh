@@ -78,12 +78,18 @@ __device__ __forceinline__ bool mu_edge(double v, double x, uint32_t hx) {
 }
 
 // v >= 0, x >= 0 (callers filter the rest); hv, hx = high words
-__device__ __forceinline__ int select_method_hw(double v, double x, uint32_t hv, uint32_t hx) {
+__device__ __forceinline__ bool is_mu_hw(double v, double x, uint32_t hv, uint32_t hx) {
     bool mu = hx > B200_HW_X30 && hv <= B200_HW_V15;                        // x > 30 && v < 15.3919
-    if (!mu && hx > B200_HW_X59) mu = (hv == 0) || mu_edge(v, x, hx);      // x > 59.6925 && (v <= 0 || edge)
-    if (mu) return M_MU;
-    if ((hx > B200_HW_X19 && hv > B200_HW_V07) || hv > B200_HW_V12) return M_U13;
-    return M_FALLBACK;
+    // x > 59.6925 && (v <= 0 || edge).  For x > 5.08 the edge implies v < x,
+    // so v >= x (hv >= hx) settles it without the logs.
+    if (!mu && hx > B200_HW_X59 && hv < hx) mu = (hv == 0) || mu_edge(v, x, hx);
+    return mu;
+}
+__device__ __forceinline__ bool is_u_hw(uint32_t hv, uint32_t hx) {
+    return (hx > B200_HW_X19 && hv > B200_HW_V07) || hv > B200_HW_V12;     // Table 1, U13 region
+}
+__device__ __forceinline__ int select_method_hw(double v, double x, uint32_t hv, uint32_t hx) {
+    return is_mu_hw(v, x, hv, hx) ? M_MU : is_u_hw(hv, hx) ? M_U13 : M_FALLBACK;
 }
 
 __device__ __forceinline__ int select_method(double v, double x) {
@@ -589,13 +595,12 @@ __device__ __forceinline__ T log_kv_integral_paper(T v, T x) {
 enum : int { E_MU = 0, E_U4 = 1, E_U6 = 2, E_U9 = 3, E_U13 = 4, E_FB_A = 5, E_FB_B = 6 };
 
 __device__ __forceinline__ int select_eval_hw(double v, double x, uint32_t hv, uint32_t hx, uint32_t hw_split) {
-    const int m = select_method_hw(v, x, hv, hx);
-    if (m == M_MU) return E_MU;
-    if (m == M_U13) {
-        const int k = select_u_terms_hw(hv, hx);
-        return k == 4 ? E_U4 : k == 6 ? E_U6 : k == 9 ? E_U9 : E_U13;
-    }
-    return hx > hw_split ? E_FB_B : E_FB_A;
+    // selects, no nested branches: U sub-bin from max(v, x) (R12), fallback cost class from x
+    const uint32_t m = hv > hx ? hv : hx;
+    const int eu = m >= B200_HW_R1800 ? E_U4 : m >= B200_HW_R280 ? E_U6 : m >= B200_HW_R80 ? E_U9 : E_U13;
+    const int ef = hx > hw_split ? E_FB_B : E_FB_A;
+    const int e = is_u_hw(hv, hx) ? eu : ef;
+    return is_mu_hw(v, x, hv, hx) ? E_MU : e;
 }
 __device__ __forceinline__ int select_eval(double v, double x, uint32_t hw_split) {
     return select_eval_hw(v, x, hiw(v), hiw(x), hw_split);
