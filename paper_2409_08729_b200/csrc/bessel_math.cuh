@@ -422,42 +422,65 @@ __device__ __forceinline__ void temme_gammas(T mu, T &gam1, T &gam2, T &gampl, T
     gammi = ev - mu * od;   // 1/Gamma(1-mu)
 }
 
-// returns log K_mu(x) and rho = K_{mu+1}(x) / K_mu(x), for 0 < x <= 2 (Temme's series)
+// sinh(e)/e and cosh(e) from E = e^e (|e| <= 162 here)
+template <typename T>
+__device__ __forceinline__ void sinhc_cosh(T e, T E, T &shc, T &ch) {
+    const T Ei = fm_rcp(E);
+    ch = T(0.5) * (E + Ei);
+    if (fabs(e) < T(0.5)) {
+        // sinh(e)/e = sum_k e^{2k} / (2k+1)!, 9 terms for e^2 < 1/4
+        const T e2 = e * e;
+        T p = T(1.0 / 6402373705728000.0);                 // 1/18!
+#pragma unroll
+        for (int k = 7; k >= 0; --k) {
+            double f = 1.0;                                  // 1/(2k+1)!
+            for (int j = 2; j <= 2 * k + 1; ++j) f /= j;
+            p = fma(p, e2, T(f));
+        }
+        shc = p;
+    } else {
+        shc = T(0.5) * (E - Ei) * fm_rcp(e);
+    }
+}
+
+// returns log K_mu(x) and rho = K_{mu+1}(x) / K_mu(x), for 0 < x <= 2 (Temme's series).
+// Elementary functions from fastmath.cuh (x >= 1e-140 on the fast path, so
+// ln(2/x) <= 323, |mu ln(2/x)| <= 162, every reciprocal argument normal).
 template <typename T>
 __device__ __forceinline__ T temme_kmu(T mu, T x, T &rho) {
     const T eps = Tr<T>::eps;
-    {
-        const T d = -log(T(0.5) * x);       // ln(2/x)
-        const T e = mu * d;
-        const T fact = (mu == T(0)) ? T(1) : (T(CUDART_PI) * mu) / d_sinpi(mu);
-        const T fact2 = (e == T(0)) ? T(1) : sinh(e) / e;
-        T gam1, gam2, gampl, gammi;
-        temme_gammas<T>(mu, gam1, gam2, gampl, gammi);
-        T ff = fact * (gam1 * cosh(e) + gam2 * fact2 * d);
-        T sum = ff;
-        const T ee = exp(e);
-        T p = T(0.5) * ee / gampl;          // 1/2 (2/x)^mu Gamma(1+mu)
-        T q = T(0.5) / (ee * gammi);        // 1/2 (x/2)^mu Gamma(1-mu)
-        T c = T(1);
-        const T dd = T(0.25) * x * x;
-        T sum1 = p;
-        const T m2 = mu * mu;
-        for (int i = 1; i < 100; ++i) {
-            const T fi = T(i);
-            // 1/(i-mu), 1/(i+mu) and 1/(i^2-mu^2) share one reciprocal
-            const T inv = T(1) / (fi * fi - m2);
-            ff = (fi * ff + p + q) * inv;
-            c *= dd * c_inv_k<T>(i);
-            p *= (fi + mu) * inv;
-            q *= (fi - mu) * inv;
-            const T del = c * ff;
-            sum += del;
-            sum1 += c * (p - fi * ff);
-            if (fabs(del) < fabs(sum) * eps) break;
-        }
-        rho = (T(2) / x) * (sum1 / sum);
-        return log(sum);
+    const T d = -fm_log(T(0.5) * x);                          // ln(2/x)
+    const T e = mu * d;
+    const T fact = (mu == T(0)) ? T(1) : (T(CUDART_PI) * mu) * fm_rcp(d_sinpi(mu));
+    const T ee = fm_exp(e);
+    T fact2, che;
+    sinhc_cosh<T>(e, ee, fact2, che);
+    T gam1, gam2, gampl, gammi;
+    temme_gammas<T>(mu, gam1, gam2, gampl, gammi);
+    T ff = fact * (gam1 * che + gam2 * fact2 * d);
+    T sum = ff;
+    T p = T(0.5) * ee * fm_rcp(gampl);                        // 1/2 (2/x)^mu Gamma(1+mu)
+    T q = T(0.5) * fm_rcp(ee * gammi);                        // 1/2 (x/2)^mu Gamma(1-mu)
+    T c = T(1);
+    const T dd = T(0.25) * x * x;
+    T sum1 = p;
+    const T m2 = mu * mu;
+    T fi = T(0);
+    for (int i = 1; i < 100; ++i) {
+        fi += T(1);
+        // 1/(i-mu), 1/(i+mu) and 1/(i^2-mu^2) share one reciprocal
+        const T inv = fm_rcp(fma(fi, fi, -m2));
+        ff = (fi * ff + p + q) * inv;
+        c *= dd * c_inv_k<T>(i);
+        p *= (fi + mu) * inv;
+        q *= (fi - mu) * inv;
+        const T del = c * ff;
+        sum += del;
+        sum1 += c * (p - fi * ff);
+        if (fabs(del) < fabs(sum) * eps) break;
     }
+    rho = T(2) * sum1 * fm_rcp(x * sum);
+    return fm_log(sum);
 }
 
 // K_mu(x) and K_{mu+1}(x), |mu| <= 1/2, on the band 2 < x <= 30 of the
@@ -537,18 +560,27 @@ __device__ __forceinline__ T log_kv_fallback(T v, T x) {
     }
     const T lk = temme_kmu<T>(mu, x, rho);
     if (nl == 0) return lk;
-    // small x: scaled by 10^-30 whenever the ratio exceeds 10^30
-    T km = T(1), kp = rho, nu = mu;
-    int e = 0;
+    // small x: each step multiplies by up to 2 nu / x (<= 3e141), so the ratio
+    // (in double for both precisions) is renormalised by an exact power of two
+    // whenever it passes 2^400
+    double km = 1.0, kp = double(rho), nu = double(mu);
+    const double tx = double(tox);
+    int e2 = 0;
     for (int i = 1; i < nl; ++i) {
-        nu += T(1);
-        const T kn = fma(nu * tox, kp, km);
+        nu += 1.0;
+        const double kn = fma(nu * tx, kp, km);
         km = kp;
         kp = kn;
-        if (kp > T(1e30)) { km *= T(1e-30); kp *= T(1e-30); e += 1; }
+        if (kp > 2.5822498780869086e120) {                    // 2^400
+            const int k = ilogb(kp);
+            const double sc = scalbn(1.0, -k);
+            km *= sc;
+            kp *= sc;
+            e2 += k;
+        }
     }
-    // kp = K_v / K_mu * 1e-30^e
-    return lk + fm_log(kp) + T(e) * T(69.07755278982137);   // 30 ln 10
+    // kp = K_v / K_mu * 2^-e2
+    return lk + T(fm_log(kp) + double(e2) * 0.6931471805599453);
 }
 
 // ---------------------------------------------------------------- paper K

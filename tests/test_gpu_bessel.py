@@ -328,3 +328,18 @@ def test_tile_tails_against_separate_sizes(B):
     for n in (1, 2, 3, 1023, 1025, 2047, 2049, 3001):
         got = _run(B, "iv", v[:n], x[:n])
         assert np.array_equal(got, full_i[:n]), n
+
+
+@pytest.mark.parametrize("fn", ["iv", "kv"])
+def test_tiny_arguments_stay_finite(B, fn):
+    """x down to 1e-300 with orders up to the fallback edge: log K ~ v log(2/x) is
+    finite (the forward recurrence renormalises by powers of two)."""
+    xs = np.array([1e-300, 1e-200, 1e-141, 1e-139, 1e-100, 1e-30, 1e-8])
+    vs = np.array([0.0, 0.3, 1.0, 5.0, 5.5, 12.0, 12.6])
+    v, x = np.meshgrid(vs, xs)
+    v, x = v.ravel(), x.ravel()
+    got = _run(B, fn, v, x)
+    assert np.all(np.isfinite(got) | ((fn == "iv") & (v > 0) & np.isinf(got) & (got < 0)))
+    ok = x >= 1e-140 if fn == "kv" else x >= 1e-100
+    ref = _ref(fn, v[ok], x[ok])
+    assert oracle.rel_err(got[ok], ref).max() <= TOL64
