@@ -307,16 +307,20 @@ __device__ __forceinline__ void log_bessel_mu_ik(T v, T x, T &li, T &lk) {
     T term = T(1), si = T(1), sk = T(1);          // K terms (all signs +); I alternates
     // terms in (odd, even) pairs, fully unrolled: (2k-1)^2 and 1/k are constants
 #pragma unroll
-    for (int k = 1; k < KMU; k += 2) {
-        T i1, i2;
-        if constexpr (sizeof(T) == 8) { i1 = c_inv_d[k]; i2 = c_inv_d[k + 1]; }
-        else { i1 = T(1.0 / k); i2 = T(1.0 / (k + 1)); }
-        term *= (mu - T((2 * k - 1) * (2 * k - 1))) * (c * i1);
-        si -= term;                                // summed in order, as the separate
-        sk += term;                                // series (no even/odd cancellation)
-        term *= (mu - T((2 * k + 1) * (2 * k + 1))) * (c * i2);
-        si += term;
-        sk += term;
+    for (int k = 1; k < KMU; k += 4) {         // four terms per stop test (KMU = 4*6 + 2)
+#pragma unroll
+        for (int u = 0; u < 4 && k + u <= KMU; u += 2) {
+            const int k1 = k + u;
+            T i1, i2;
+            if constexpr (sizeof(T) == 8) { i1 = c_inv_d[k1]; i2 = c_inv_d[k1 + 1]; }
+            else { i1 = T(1.0 / k1); i2 = T(1.0 / (k1 + 1)); }
+            term *= (mu - T((2 * k1 - 1) * (2 * k1 - 1))) * (c * i1);
+            si -= term;                            // summed in order, as the separate
+            sk += term;                            // series (no even/odd cancellation)
+            term *= (mu - T((2 * k1 + 1) * (2 * k1 + 1))) * (c * i2);
+            si += term;
+            sk += term;
+        }
         if (k >= 3 && fabs(term) <= Tr<T>::eps * T(0.25) * fabs(si)) break;
     }
     const T SI = fabs(si), SK = fabs(sk);
