@@ -480,8 +480,8 @@ static int launch_eval(const T *v, const T *x, T *out, int64_t n, cudaStream_t s
 // stream: H2D(v,x) -> kernel -> D2H(out).  Copies of one slot overlap the
 // kernel of another and the two copy directions run on separate engines.
 struct HostPipe {
-    static constexpr int NSLOT = 3;
-    static constexpr int64_t CH = int64_t(1) << 23;   // 8M pairs per chunk
+    static constexpr int NSLOT = 4;
+    static constexpr int64_t CH = int64_t(1) << 21;   // 2M pairs per chunk (short pipeline fill)
     std::mutex mu;
     int dev = -1;
     cudaStream_t st[NSLOT] = {};
