@@ -118,19 +118,23 @@ template <> struct Big<float> { static constexpr float v = 1e18f; };
 // also be calculated recursively", line 208):
 //   term_k = term_{k-1} * s (mu - (2k-1)^2) / (8 x k),  s = -1 (I), +1 (K),
 // fully unrolled so (2k-1)^2 and 1/k are compile-time constants; the stop
-// test runs every second term.
+// test runs every fourth term.
 template <typename T, bool IS_K>
 __device__ __forceinline__ T mu_series(T v, T rx) {
     const T mu = T(4) * v * v;
     const T c = (IS_K ? T(0.125) : T(-0.125)) * rx;
     T term = T(1), s = T(1);
 #pragma unroll
-    for (int k = 1; k <= KMU; ++k) {
-        T inv_k;
-        if constexpr (sizeof(T) == 8) inv_k = c_inv_d[k]; else inv_k = T(1.0 / k);
-        term *= (mu - T((2 * k - 1) * (2 * k - 1))) * (c * inv_k);
-        s += term;
-        if ((k & 1) == 0 && k >= 4 && fabs(term) <= Tr<T>::eps * T(0.25) * fabs(s)) break;
+    for (int k = 1; k <= KMU; k += 4) {        // four terms per stop test
+#pragma unroll
+        for (int u = 0; u < 4 && k + u <= KMU; ++u) {
+            const int kk = k + u;
+            T inv_k;
+            if constexpr (sizeof(T) == 8) inv_k = c_inv_d[kk]; else inv_k = T(1.0 / kk);
+            term *= (mu - T((2 * kk - 1) * (2 * kk - 1))) * (c * inv_k);
+            s += term;
+        }
+        if (k >= 4 && fabs(term) <= Tr<T>::eps * T(0.25) * fabs(s)) break;
     }
     return fabs(s);
 }
