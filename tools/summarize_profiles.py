@@ -125,6 +125,7 @@ def main():
             fn = {"0": "log_iv", "1": "log_kv", "3": "log_ivkv"}.get(m.group(1)) if m else None
             if fn and "double" in e["kernel"] and "bessel_eval_kernel" in e["kernel"] and e.get("fp64_flop_per_eval"):
                 counts[fn] = {"fp64_flop_per_eval": e["fp64_flop_per_eval"],
+                              "fp64_inst_per_eval": sum(e.get(f"{k}_per_eval", 0.0) for k in ("dadd", "dmul", "dfma")),
                               "per": "pair (log I and log K)" if fn == "log_ivkv" else "evaluation",
                               "dram_bytes_per_eval": e.get("dram_bytes_per_eval"),
                               "source": f"profiles/{tag}/ncu_full.json ({e['pairs']} pairs, bench grid)"}
