@@ -343,3 +343,20 @@ def test_tiny_arguments_stay_finite(B, fn):
     ok = x >= 1e-140 if fn == "kv" else x >= 1e-100
     ref = _ref(fn, v[ok], x[ok])
     assert oracle.rel_err(got[ok], ref).max() <= TOL64
+
+
+def test_full_bench_grid_fused_sampled(B):
+    """The bench step itself: b200_log_ivkv_f64 over the full configs[1]/[2] grid
+    (11 x 20M pairs) in the bench launch configuration; all outputs finite, 20k
+    sampled pairs of both results against the oracle."""
+    dev = torch.device("cuda:0")
+    v, x = workloads.bench_grid(20_000_000, seed=0, device=dev)
+    oi, ok = B.log_ivkv(v, x)
+    torch.cuda.synchronize()
+    assert bool(torch.isfinite(oi).all()) and bool(torch.isfinite(ok).all())
+    idx = torch.randint(0, v.numel(), (20_000,), generator=torch.Generator().manual_seed(3)).to(dev)
+    vs, xs = v[idx].cpu().numpy(), x[idx].cpu().numpy()
+    assert oracle.rel_err(oi[idx].cpu().numpy(), oracle.log_iv(vs, xs)).max() <= TOL64
+    assert oracle.rel_err(ok[idx].cpu().numpy(), oracle.log_kv(vs, xs)).max() <= TOL64
+    del v, x, oi, ok
+    torch.cuda.empty_cache()
