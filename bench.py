@@ -232,6 +232,15 @@ def run_extra(args, B, workloads, ws, rank, dev, stream, dist):
         "value": 2 * nv * nx * reps / (ms / 1e3) / 1e9, "unit": UNIT, "ms_per_pass": ms / reps,
         "nonfinite_outputs": bad, "scaling": "strong"}
     del sv, sx, oi, ok
+    # -- configs[2] fp32 variant: the bench grid in float32, fused pass
+    v32, x32 = workloads.bench_grid(args.n_per_v, seed=rank, device=dev, dtype=torch.float32)
+    o1, o2 = torch.empty_like(v32), torch.empty_like(v32)
+    B.log_ivkv(v32, x32, o1, o2)
+    ms = _timed(lambda: B.log_ivkv(v32, x32, o1, o2), 3, stream, dist)
+    out["fp32_fused"] = {"config": "configs[2] fp32 variant: bench grid in float32, b200_log_ivkv_f32",
+                         "value": 2 * v32.numel() * ws * 3 / (ms / 1e3) / 1e9, "unit": UNIT,
+                         "ms_per_step": ms / 3, "dtype": "f32"}
+    del v32, x32, o1, o2
     # -- configs[4]: vMF MLE on 50000 x d features (f32), rows sharded
     n = 50_000
     lo, hi = shard_range(n, ws, rank)
@@ -368,8 +377,9 @@ def run_ours(args):
     cnt = _roofline_counts().get("log_ivkv", {})
     fl = cnt.get("fp64_flop_per_eval")         # per pair (two evaluations)
     if cnt.get("dram_bytes_per_eval"):
-        roof["traffic"] = cnt["dram_bytes_per_eval"]
-        roof["traffic_source"] = cnt["source"] + "; DRAM bytes per pair (ncu), algorithmic: 32"
+        roof["traffic"] = cnt["dram_bytes_per_eval"] * n          # bytes per launch of this step
+        roof["traffic_source"] = (cnt["source"] + f"; dram read+write {cnt['dram_bytes_per_eval']:.2f} B per pair "
+                                  f"(ncu) x {n} pairs; algorithmic {BYTES_PER_PAIR} B per pair")
     if fl and fp64_peak:
         tf = fl * n / (kms / 1e3) / 1e12
         if tf / fp64_peak > gbs / hbm_peak:
