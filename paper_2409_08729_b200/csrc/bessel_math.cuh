@@ -39,8 +39,11 @@ template <> struct Tr<float> {
 // 1/k for k = 1..400 (recurrences divide by the term index)
 #define B200_NINV 400
 static __constant__ double c_inv_d[B200_NINV + 1] = B200_INV_INIT;
+static __constant__ float c_inv_f[B200_NINV + 1] = B200_INV_INIT;
 template <typename T>
-__device__ __forceinline__ T c_inv_k(int k) { return T(c_inv_d[k]); }
+__device__ __forceinline__ T c_inv_k(int k) {
+    if constexpr (sizeof(T) == 8) return c_inv_d[k]; else return c_inv_f[k];
+}
 
 // Overload helpers so templates pick the right precision.
 __device__ __forceinline__ double d_sinpi(double a) { return sinpi(a); }
@@ -129,8 +132,7 @@ __device__ __forceinline__ T mu_series(T v, T rx) {
 #pragma unroll
         for (int u = 0; u < 4 && k + u <= KMU; ++u) {
             const int kk = k + u;
-            T inv_k;
-            if constexpr (sizeof(T) == 8) inv_k = c_inv_d[kk]; else inv_k = T(1.0 / kk);
+            const T inv_k = c_inv_k<T>(kk);
             term *= (mu - T((2 * kk - 1) * (2 * kk - 1))) * (c * inv_k);
             s += term;
         }
@@ -315,9 +317,7 @@ __device__ __forceinline__ void log_bessel_mu_ik(T v, T x, T &li, T &lk) {
 #pragma unroll
         for (int u = 0; u < 4 && k + u <= KMU; u += 2) {
             const int k1 = k + u;
-            T i1, i2;
-            if constexpr (sizeof(T) == 8) { i1 = c_inv_d[k1]; i2 = c_inv_d[k1 + 1]; }
-            else { i1 = T(1.0 / k1); i2 = T(1.0 / (k1 + 1)); }
+            const T i1 = c_inv_k<T>(k1), i2 = c_inv_k<T>(k1 + 1);
             term *= (mu - T((2 * k1 - 1) * (2 * k1 - 1))) * (c * i1);
             si -= term;                            // summed in order, as the separate
             sk += term;                            // series (no even/odd cancellation)

@@ -17,7 +17,7 @@ SETS = [
 ]
 
 
-def run(n=4_000_000, fused=False):
+def run(n=4_000_000, fused=False, dtype="f64"):
     import torch
     sys.path.insert(0, ".")
     import paper_2409_08729_b200 as B
@@ -26,6 +26,8 @@ def run(n=4_000_000, fused=False):
     for name, (v0, v1), (x0, x1) in SETS:
         v = torch.empty(n, dtype=torch.float64, device=dev).uniform_(v0, v1, generator=g)
         x = torch.empty(n, dtype=torch.float64, device=dev).uniform_(x0, x1, generator=g)
+        if dtype == "f32":
+            v, x = v.float(), x.float()
         if fused:
             B.log_ivkv(v, x)
         else:
@@ -71,10 +73,11 @@ def parse(rep, n=4_000_000, fused=False):
 
 if __name__ == "__main__":
     fz = "--fused" in sys.argv
-    args = [a for a in sys.argv[1:] if a != "--fused"]
+    dt = "f32" if "--f32" in sys.argv else "f64"
+    args = [a for a in sys.argv[1:] if a not in ("--fused", "--f32")]
     if args and args[0] == "parse":
         r = parse(args[1], fused=fz)
         if len(args) > 2:
             json.dump(r, open(args[2], "w"), indent=1)
     else:
-        run(fused=fz)
+        run(fused=fz, dtype=dt)
