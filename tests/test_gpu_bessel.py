@@ -360,3 +360,20 @@ def test_full_bench_grid_fused_sampled(B):
     assert oracle.rel_err(ok[idx].cpu().numpy(), oracle.log_kv(vs, xs)).max() <= TOL64
     del v, x, oi, ok
     torch.cuda.empty_cache()
+
+
+def test_c_abi_from_plain_c(B, tmp_path):
+    """The shared library used from C (tools/capi_example.c): device and host-buffer
+    entry points against the half-integer closed forms, argument errors reported."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    libdir = os.path.join(root, "paper_2409_08729_b200", "lib")
+    exe = str(tmp_path / "capi_example")
+    subprocess.check_call(["nvcc", "-Wno-deprecated-gpu-targets", "-o", exe,
+                           os.path.join(root, "tools", "capi_example.c"),
+                           "-I" + os.path.join(root, "include"), "-L" + libdir, "-lbessel_b200",
+                           "-Xlinker", "-rpath=" + libdir])
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "max rel err" in r.stdout
