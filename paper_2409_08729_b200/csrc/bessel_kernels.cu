@@ -434,18 +434,6 @@ __global__ void classify_kernel(const double *__restrict__ v, const double *__re
 }
 
 // ------------------------------------------------------------------ launch
-static int g_num_sms = 0;
-static std::once_flag g_dev_once;
-
-static int device_sms() {
-    std::call_once(g_dev_once, [] {
-        int dev = 0;
-        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
-    });
-    return g_num_sms;
-}
-
 template <typename T, int FN>
 static int launch_eval(const T *v, const T *x, T *out, int64_t n, cudaStream_t s, T *out2 = nullptr) {
     if (n < 0) return set_err(B200_ERR_INVALID_ARGUMENT, "n < 0");
@@ -455,17 +443,25 @@ static int launch_eval(const T *v, const T *x, T *out, int64_t n, cudaStream_t s
     const bool tma = ((reinterpret_cast<uintptr_t>(v) | reinterpret_cast<uintptr_t>(x) |
                        reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(out2)) & 15) == 0;
     constexpr int SMEM = smem_bytes<T, FN>();
-    static int occ[2] = {0, 0};
-    if (occ[tma] == 0) {
+    // the dynamic-shared-memory opt-in and the occupancy are per device
+    constexpr int MAXDEV = 64;
+    static std::atomic<int> occ[2][MAXDEV];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= MAXDEV)
+        return set_err(B200_ERR_NO_DEVICE, "no current CUDA device (or device id >= 64)");
+    int o = occ[tma][dev].load(std::memory_order_relaxed);
+    if (o == 0) {
         auto kern = tma ? bessel_eval_kernel<T, FN, true> : bessel_eval_kernel<T, FN, false>;
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
         if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute");
-        int o = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, kern, TPB, SMEM);
-        occ[tma] = o > 0 ? o : 1;
+        if (o <= 0) o = 1;
+        occ[tma][dev].store(o, std::memory_order_relaxed);
     }
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
     const int64_t ntiles = (n + TILE - 1) / TILE;
-    const int64_t resident = int64_t(device_sms()) * occ[tma];
+    const int64_t resident = int64_t(sms) * o;
     const int grid = int(ntiles < resident ? ntiles : resident);
     if (tma)
         bessel_eval_kernel<T, FN, true><<<grid, TPB, SMEM, s>>>(v, x, out, out2, n);
