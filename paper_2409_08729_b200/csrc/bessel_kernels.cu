@@ -1,16 +1,21 @@
 // bessel_kernels.cu -- sm_100a kernels and the C ABI of include/bessel_b200.h.
 //
 // Hot path: batched log I_v(x) / log K_v(x) (§3-§4).  One persistent
-// kernel per (function, precision).  Each CTA processes tiles of TILE pairs:
-//   1. coalesced load of (v, x) into registers, region id per element
-//      (Algorithm 1 with the GPU branch set, plus a cost sub-bin);
-//   2. an in-CTA counting sort of the tile by bin (packed 12-bit counters,
-//      warp-shuffle scan) into shared memory -- the paper's "sort the input
-//      elements based on which expression is used" (§4.3) done
-//      per tile in SMEM instead of as a global sort, so no extra HBM pass;
-//   3. every warp evaluates 32 consecutive binned elements (warp-uniform
-//      method except at <= NBIN-1 bin boundaries per tile);
-//   4. results scattered back to tile order in SMEM, coalesced store.
+// kernel per (function, precision, alignment); FN_IK evaluates both functions
+// of each pair in one pass.  Each CTA processes tiles of TILE pairs:
+//   0. one thread requests the NEXT tile with a bulk copy (TMA) into the other
+//      half of a double-buffered shared-memory stage (per-thread cp.async for
+//      8-byte-aligned pointers);
+//   1. every thread classifies its elements (Algorithm 1 with the GPU branch
+//      set plus cost sub-bins, integer predicates on IEEE high words);
+//   2. an in-CTA counting sort of the element indices by bin (packed 8-bit
+//      counters, warp-shuffle scans) -- the paper's "sort the input elements
+//      based on which expression is used" (§4.3) done per tile in
+//      shared memory instead of as a global sort, so no extra HBM pass;
+//   3. every warp evaluates 32 consecutive sorted slots (warp-uniform method
+//      except at <= 7 bin boundaries per tile), gathering (v, x) from the stage
+//      and writing the results in tile order;
+//   4. one thread stores the results with a bulk copy.
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -44,7 +49,7 @@ constexpr int TPB = B200_TPB;
 constexpr int ITEMS = B200_ITEMS;
 constexpr int TILE = TPB * ITEMS;       // 1024 pairs per tile
 static_assert(TILE <= 4096, "s_idx packs a 12-bit tile index with the bin");
-constexpr int BIN_SLOW = 7;
+constexpr int BIN_SLOW = 7;           // out-of-range / special inputs (slow_eval)
 
 std::atomic<int64_t> g_launches{0};
 static thread_local char g_err[256] = "";

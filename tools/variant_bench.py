@@ -28,7 +28,8 @@ def build(specs):
     procs = []
     for spec in specs:
         name, _, flags = spec.partition("=")
-        defs = [f"-D{f}" for f in flags.split(",") if f]
+        # items starting with '+' are raw nvcc flags ('+' stripped, '=' kept), the rest macros
+        defs = [f[1:] if f.startswith("+") else f"-D{f}" for f in flags.split(",") if f]
         cmd = [_build.nvcc()] + _build.NVCC_FLAGS + defs + ["-o", os.path.join(OUT, name + ".so")] + \
               [os.path.join(_build.CSRC, s) for s in _build.SOURCES]
         procs.append((name, subprocess.Popen(cmd)))
