@@ -377,3 +377,21 @@ def test_c_abi_from_plain_c(B, tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "max rel err" in r.stdout
+
+
+def test_fused_deterministic_and_on_side_stream(B):
+    """Same inputs, same bits (fixed per-element evaluation order); the kernels run on
+    the caller's current stream (a side stream here) and honour its ordering."""
+    v, x = workloads.bench_grid_numpy(20_000, seed=42)
+    vt, xt = _dev(v), _dev(x)
+    a = B.log_ivkv(vt, xt)
+    b = B.log_ivkv(vt, xt)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        vs, xs = vt.clone(), xt.clone()        # produced on the side stream
+        c = B.log_ivkv(vs, xs)
+        ci = B.log_iv(vs, xs)
+    s.synchronize()
+    assert torch.equal(c[0], a[0]) and torch.equal(c[1], a[1])
+    assert oracle.rel_err(ci.cpu().numpy(), oracle.log_iv(v, x)).max() <= TOL64
