@@ -20,6 +20,7 @@ static __constant__ float c_uk_f[B200_UK_NCOEF] = B200_UK_TABLE_INIT;
 static __constant__ double c_rg_d[B200_RGAMMA_NT] = B200_RGAMMA_INIT;
 static __constant__ float c_rg_f[B200_RGAMMA_NT] = B200_RGAMMA_INIT;
 static __constant__ double c_eta_d[B200_ETA_NT] = B200_ETA_TAYLOR_INIT;
+static __constant__ double c_sinpi_d[B200_SINPI_NT] = B200_SINPI_INIT;
 static __constant__ float c_eta_f[B200_ETA_NT] = B200_ETA_TAYLOR_INIT;
 
 template <typename T> struct Tr;
@@ -375,10 +376,12 @@ __device__ __forceinline__ T log_iv_series(T v, T x) {
         const T mu = v - fl;
         const int nl = int(fl);
         T pr = T(1), m = mu;
-        for (int j = 0; j < nl; ++j) {
-            m += T(1);
-            pr *= m;
+        for (int j = 1; j < nl; j += 2) {      // factor pairs (mu+j)(mu+j+1)
+            const T a = m + T(1);
+            m += T(2);
+            pr *= a * m;
         }
+        if (nl & 1) pr *= m + T(1);
         T g = T(c_rg_d[B200_RGAMMA_NT - 1]);
 #pragma unroll
         for (int j = B200_RGAMMA_NT - 2; j >= 0; --j) g = fma(g, mu, T(c_rg_d[j]));
@@ -459,7 +462,12 @@ __device__ __forceinline__ T temme_kmu(T mu, T x, T &rho) {
     const T eps = Tr<T>::eps;
     const T d = -fm_log(T(0.5) * x);                          // ln(2/x)
     const T e = mu * d;
-    const T fact = (mu == T(0)) ? T(1) : (T(CUDART_PI) * mu) * fm_rcp(d_sinpi(mu));
+    // pi mu / sin(pi mu) = 1 / sum_k SINPI[k] mu^(2k)  (|mu| <= 1/2, tables.h)
+    const T m2 = mu * mu;
+    T sp = T(c_sinpi_d[B200_SINPI_NT - 1]);
+#pragma unroll
+    for (int k = B200_SINPI_NT - 2; k >= 0; --k) sp = fma(sp, m2, T(c_sinpi_d[k]));
+    const T fact = fm_rcp(sp);
     const T ee = fm_exp(e);
     T fact2, che;
     sinhc_cosh<T>(e, ee, fact2, che);
@@ -472,19 +480,22 @@ __device__ __forceinline__ T temme_kmu(T mu, T x, T &rho) {
     T c = T(1);
     const T dd = T(0.25) * x * x;
     T sum1 = p;
-    const T m2 = mu * mu;
     T fi = T(0);
-    for (int i = 1; i < 100; ++i) {
-        fi += T(1);
-        // 1/(i-mu), 1/(i+mu) and 1/(i^2-mu^2) share one reciprocal
-        const T inv = fm_rcp(fma(fi, fi, -m2));
-        ff = (fi * ff + p + q) * inv;
-        c *= dd * c_inv_k<T>(i);
-        p *= (fi + mu) * inv;
-        q *= (fi - mu) * inv;
-        const T del = c * ff;
-        sum += del;
-        sum1 += c * (p - fi * ff);
+    for (int i = 1; i < 100; i += 2) {          // two terms per stop test
+        T del;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            fi += T(1);
+            // 1/(i-mu), 1/(i+mu) and 1/(i^2-mu^2) share one reciprocal
+            const T inv = fm_rcp(fma(fi, fi, -m2));
+            ff = (fi * ff + p + q) * inv;
+            c *= dd * c_inv_k<T>(i + u);
+            p *= (fi + mu) * inv;
+            q *= (fi - mu) * inv;
+            del = c * ff;
+            sum += del;
+            sum1 += c * (p - fi * ff);
+        }
         if (fabs(del) < fabs(sum) * eps) break;
     }
     rho = T(2) * sum1 * fm_rcp(x * sum);
@@ -574,17 +585,27 @@ __device__ __forceinline__ T log_kv_fallback(T v, T x) {
     double km = 1.0, kp = double(rho), nu = double(mu);
     const double tx = double(tox);
     int e2 = 0;
-    for (int i = 1; i < nl; ++i) {
-        nu += 1.0;
-        const double kn = fma(nu * tx, kp, km);
-        km = kp;
-        kp = kn;
-        if (kp > 2.5822498780869086e120) {                    // 2^400
-            const int k = ilogb(kp);
-            const double sc = scalbn(1.0, -k);
-            km *= sc;
-            kp *= sc;
-            e2 += k;
+    if (x >= T(1e-6)) {
+        // (2 * 13 / 1e-6)^13 < 2^400: no renormalisation needed
+        for (int i = 1; i < nl; ++i) {
+            nu += 1.0;
+            const double kn = fma(nu * tx, kp, km);
+            km = kp;
+            kp = kn;
+        }
+    } else {
+        for (int i = 1; i < nl; ++i) {
+            nu += 1.0;
+            const double kn = fma(nu * tx, kp, km);
+            km = kp;
+            kp = kn;
+            if (kp > 2.5822498780869086e120) {                // 2^400
+                const int k = ilogb(kp);
+                const double sc = scalbn(1.0, -k);
+                km *= sc;
+                kp *= sc;
+                e2 += k;
+            }
         }
     }
     // kp = K_v / K_mu * 2^-e2

@@ -139,6 +139,17 @@ def hiword(c: float) -> int:
     return struct.unpack("<Q", struct.pack("<d", c))[0] >> 32
 
 
+SINPI_NT = 12
+
+
+def sinpi_taylor(n: int = SINPI_NT):
+    """c_k with sin(pi z) / (pi z) = sum_k c_k z^(2k), c_k = (-1)^k pi^(2k) / (2k+1)!
+    (mpmath, 60 digits); 12 terms give 2^-60 for |z| <= 1/2."""
+    import mpmath
+    mpmath.mp.dps = 60
+    return [float((-1) ** k * mpmath.pi ** (2 * k) / mpmath.factorial(2 * k + 1)) for k in range(n)]
+
+
 def render() -> str:
     lines = [
         "// GENERATED by paper_2409_08729_b200/gen_tables.py -- do not edit.",
@@ -176,6 +187,10 @@ def render() -> str:
     lines.append("// f64 exp table: 2^(j/%d) hi, lo" % EXP_TAB_N)
     lines.append("#define B200_EXP_TAB_N %d" % EXP_TAB_N)
     lines.append("#define B200_EXPTAB_INIT_STRUCT { %s }" % ", ".join("{%.17e, %.17e}" % r for r in exp_table()))
+    lines.append("")
+    lines.append("// sin(pi z)/(pi z) = sum_k SINPI[k] z^(2k) (|z| <= 1/2), mpmath 60 digits")
+    lines.append("#define B200_SINPI_NT %d" % SINPI_NT)
+    lines.append("#define B200_SINPI_INIT { %s }" % ", ".join("%.17e" % c for c in sinpi_taylor()))
     lines.append("")
     lines.append("// dispatch thresholds: IEEE high words (gen_tables.THRESHOLDS)")
     for k, c in THRESHOLDS.items():
