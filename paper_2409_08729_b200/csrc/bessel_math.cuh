@@ -47,8 +47,6 @@ __device__ __forceinline__ T c_inv_k(int k) {
 }
 
 // Overload helpers so templates pick the right precision.
-__device__ __forceinline__ double d_sinpi(double a) { return sinpi(a); }
-__device__ __forceinline__ float d_sinpi(float a) { return sinpif(a); }
 __device__ __forceinline__ double d_lgamma(double a) { return lgamma(a); }
 __device__ __forceinline__ float d_lgamma(float a) { return lgammaf(a); }
 
