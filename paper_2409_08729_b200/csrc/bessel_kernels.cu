@@ -43,11 +43,14 @@ namespace b200 {
 #define B200_MINB_IK 4       // CTAs per SM for the fused I + K pass
 #endif
 #ifndef B200_ITEMS
-#define B200_ITEMS 4
+#define B200_ITEMS 6         // elements per thread per tile (tile = 1536 pairs)
+#endif
+#ifndef B200_INPLACE
+#define B200_INPLACE 1       // results overwrite the stage slots of their own elements
 #endif
 constexpr int TPB = B200_TPB;
 constexpr int ITEMS = B200_ITEMS;
-constexpr int TILE = TPB * ITEMS;       // 1024 pairs per tile
+constexpr int TILE = TPB * ITEMS;       // 1536 pairs per tile
 static_assert(TILE <= 4096, "s_idx packs a 12-bit tile index with the bin");
 constexpr int BIN_SLOW = 7;           // out-of-range / special inputs (slow_eval)
 
@@ -244,7 +247,13 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 //      through the index and writing the result to s_res in tile order;
 //   4. (one thread) bulk store of s_res to HBM.
 template <typename T, int FN>
-constexpr int smem_bytes() { return (4 + (FN == FN_IK ? 2 : 1)) * TILE * int(sizeof(T)) + TILE * 2; }
+constexpr int smem_bytes() {
+#if B200_INPLACE
+    return 4 * TILE * int(sizeof(T)) + TILE * 2;           // results overwrite the stage
+#else
+    return (4 + (FN == FN_IK ? 2 : 1)) * TILE * int(sizeof(T)) + TILE * 2;
+#endif
+}
 
 template <typename T, int FN, bool TMA>
 __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B200_MINB_IK : B200_MINB_K)
@@ -254,8 +263,10 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
     // dynamic shared memory (smem_bytes<T, FN>()): stage[2][2][TILE], res[NOUT][TILE], idx[TILE]
     extern __shared__ __align__(128) unsigned char s_dyn[];
     auto s_stage = reinterpret_cast<T (*)[2][TILE]>(s_dyn);                       // [buffer][v|x][element]
+#if !B200_INPLACE
     auto s_res = reinterpret_cast<T (*)[TILE]>(s_dyn + 4 * TILE * sizeof(T));     // [output][element]
-    uint16_t *s_idx = reinterpret_cast<uint16_t *>(s_dyn + (4 + NOUT) * TILE * sizeof(T));
+#endif
+    uint16_t *s_idx = reinterpret_cast<uint16_t *>(s_dyn + (4 + (B200_INPLACE ? 0 : NOUT)) * TILE * sizeof(T));
     __shared__ uint64_t s_wtot[TPB / 32];             // per-warp bin totals, 8-bit fields
     __shared__ alignas(8) uint64_t s_bar[2];
 
@@ -270,6 +281,9 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
         if constexpr (TMA) {
             if (tid == 0) {
                 const int ra = rem & ~(VEC - 1);                  // bulk part (multiple of 16 bytes)
+#if B200_INPLACE
+                bulk_wait_read();                                 // buffer's results (2 tiles ago) stored
+#endif
                 fence_proxy_async();
                 mbar_expect_tx(&s_bar[buf], uint32_t(2 * ra * sizeof(T)));
                 if (ra > 0) {
@@ -309,6 +323,9 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
         if (tile + gridDim.x < ntiles) issue(tile + gridDim.x, buf ^ 1);
         // 1. wait for this tile, bin the owned elements
         T *sv = s_stage[buf][0], *sx = s_stage[buf][1];
+#if B200_INPLACE
+        T *s_res[2] = {sv, sx};                    // results overwrite (v, x) of their own element
+#endif
         if constexpr (TMA) {
             mbar_wait(&s_bar[buf], parity[buf]);
             parity[buf] ^= 1u;
@@ -381,9 +398,11 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
                 s_idx[pos] = uint16_t((tid + i * TPB) | (b << 12));   // tile index | bin
             }
         }
+#if !B200_INPLACE
         if constexpr (TMA) {
             if (tid == 0) bulk_wait_read();    // the previous tile's stores have read s_res
         }
+#endif
         __syncthreads();
         // 3. evaluate: sorted slot p -> element j of the stage (warp w takes the
         //    32-slot chunks w, w + 8, w + 16, w + 24: the expensive high bins at
