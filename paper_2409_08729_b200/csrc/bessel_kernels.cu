@@ -45,9 +45,6 @@ namespace b200 {
 #ifndef B200_ITEMS
 #define B200_ITEMS 6         // elements per thread per tile (tile = 1536 pairs)
 #endif
-#ifndef B200_INPLACE
-#define B200_INPLACE 1       // results overwrite the stage slots of their own elements
-#endif
 constexpr int TPB = B200_TPB;
 constexpr int ITEMS = B200_ITEMS;
 constexpr int TILE = TPB * ITEMS;       // 1536 pairs per tile
@@ -244,29 +241,22 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 //      totals, no extra barrier);
 //   3. every warp evaluates 32 consecutive sorted slots (warp-uniform method
 //      except at <= 7 bin boundaries per tile), reading (v, x) from the stage
-//      through the index and writing the result to s_res in tile order;
-//   4. (one thread) bulk store of s_res to HBM.
+//      through the index and writing the result(s) over that element's own
+//      (v, x) slots (each element is read and written by one thread only);
+//   4. (one thread) bulk store of the stage's result arrays to HBM; the
+//      buffer is reloaded only after the store has read it.
 template <typename T, int FN>
-constexpr int smem_bytes() {
-#if B200_INPLACE
-    return 4 * TILE * int(sizeof(T)) + TILE * 2;           // results overwrite the stage
-#else
-    return (4 + (FN == FN_IK ? 2 : 1)) * TILE * int(sizeof(T)) + TILE * 2;
-#endif
-}
+constexpr int smem_bytes() { return 4 * TILE * int(sizeof(T)) + TILE * 2; }   // stage[2][2][TILE] + idx[TILE]
 
 template <typename T, int FN, bool TMA>
 __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B200_MINB_IK : B200_MINB_K)
     bessel_eval_kernel(const T *__restrict__ vin, const T *__restrict__ xin, T *__restrict__ out,
                        T *__restrict__ out2, int64_t n) {
     constexpr int NOUT = FN == FN_IK ? 2 : 1;         // results per element (out, out2)
-    // dynamic shared memory (smem_bytes<T, FN>()): stage[2][2][TILE], res[NOUT][TILE], idx[TILE]
+    // dynamic shared memory (smem_bytes<T, FN>()): stage[2][2][TILE], idx[TILE]
     extern __shared__ __align__(128) unsigned char s_dyn[];
     auto s_stage = reinterpret_cast<T (*)[2][TILE]>(s_dyn);                       // [buffer][v|x][element]
-#if !B200_INPLACE
-    auto s_res = reinterpret_cast<T (*)[TILE]>(s_dyn + 4 * TILE * sizeof(T));     // [output][element]
-#endif
-    uint16_t *s_idx = reinterpret_cast<uint16_t *>(s_dyn + (4 + (B200_INPLACE ? 0 : NOUT)) * TILE * sizeof(T));
+    uint16_t *s_idx = reinterpret_cast<uint16_t *>(s_dyn + 4 * TILE * sizeof(T));
     __shared__ uint64_t s_wtot[TPB / 32];             // per-warp bin totals, 8-bit fields
     __shared__ alignas(8) uint64_t s_bar[2];
 
@@ -281,9 +271,7 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
         if constexpr (TMA) {
             if (tid == 0) {
                 const int ra = rem & ~(VEC - 1);                  // bulk part (multiple of 16 bytes)
-#if B200_INPLACE
-                bulk_wait_read();                                 // buffer's results (2 tiles ago) stored
-#endif
+                bulk_wait_read();                                 // this buffer's results (2 tiles ago) are out
                 fence_proxy_async();
                 mbar_expect_tx(&s_bar[buf], uint32_t(2 * ra * sizeof(T)));
                 if (ra > 0) {
@@ -323,9 +311,7 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
         if (tile + gridDim.x < ntiles) issue(tile + gridDim.x, buf ^ 1);
         // 1. wait for this tile, bin the owned elements
         T *sv = s_stage[buf][0], *sx = s_stage[buf][1];
-#if B200_INPLACE
         T *s_res[2] = {sv, sx};                    // results overwrite (v, x) of their own element
-#endif
         if constexpr (TMA) {
             mbar_wait(&s_bar[buf], parity[buf]);
             parity[buf] ^= 1u;
@@ -398,11 +384,6 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
                 s_idx[pos] = uint16_t((tid + i * TPB) | (b << 12));   // tile index | bin
             }
         }
-#if !B200_INPLACE
-        if constexpr (TMA) {
-            if (tid == 0) bulk_wait_read();    // the previous tile's stores have read s_res
-        }
-#endif
         __syncthreads();
         // 3. evaluate: sorted slot p -> element j of the stage (warp w takes the
         //    32-slot chunks w, w + 8, w + 16, w + 24: the expensive high bins at
