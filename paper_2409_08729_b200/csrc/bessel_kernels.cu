@@ -106,20 +106,6 @@ __device__ __noinline__ T slow_eval(T v, T x) {
     }
 }
 
-// mu / U bins only (bin <= E_U13)
-template <typename T, int FN>
-__device__ __forceinline__ T eval_main(int bin, T v, T x) {
-    constexpr bool K = FN != FN_I;
-    if (K) v = fabs(v);
-    switch (bin) {
-        case E_MU: return log_bessel_mu<T, K, false>(v, x);
-        case E_U4: return log_bessel_u<T, K, 4, false>(v, x);
-        case E_U6: return log_bessel_u<T, K, 6, false>(v, x);
-        case E_U9: return log_bessel_u<T, K, 9, false>(v, x);
-        default: return log_bessel_u<T, K, 13, false>(v, x);
-    }
-}
-
 template <typename T, int FN>
 __device__ __forceinline__ T eval_bin(int bin, T v, T x) {
 #ifdef B200_EVAL_NOP
@@ -484,33 +470,31 @@ struct HostPipe {
     static constexpr int NSLOT = 4;
     static constexpr int64_t CH = int64_t(1) << 21;   // 2M pairs per chunk (short pipeline fill)
     std::mutex mu;
-    int dev = -1;
+    bool ready = false;
     cudaStream_t st[NSLOT] = {};
     void *buf[NSLOT] = {};   // 4 arrays of CH doubles per slot: v, x, out, out2
 };
-static HostPipe g_pipe;
+// one pipeline per device, created on first use and kept for the process lifetime
+constexpr int PIPE_MAXDEV = 64;
+static HostPipe g_pipes[PIPE_MAXDEV];
 
 template <int FN>
 static int host_eval_f64(const double *v_h, const double *x_h, double *out_h, int64_t n, double *out2_h = nullptr) {
     if (n < 0) return set_err(B200_ERR_INVALID_ARGUMENT, "n < 0");
     if (n == 0) return B200_OK;
     if (!v_h || !x_h || !out_h || (FN == FN_IK && !out2_h)) return set_err(B200_ERR_INVALID_ARGUMENT, "null pointer");
-    std::lock_guard<std::mutex> lk(g_pipe.mu);
     int dev = 0;
     int rc = cuda_err(cudaGetDevice(&dev), "cudaGetDevice");
     if (rc) return rc;
-    if (g_pipe.dev != dev) {
-        for (int i = 0; i < HostPipe::NSLOT; ++i) {
-            if (g_pipe.buf[i]) cudaFree(g_pipe.buf[i]);
-            if (g_pipe.st[i]) cudaStreamDestroy(g_pipe.st[i]);
-            g_pipe.buf[i] = nullptr;
-            g_pipe.st[i] = nullptr;
-        }
+    if (dev < 0 || dev >= PIPE_MAXDEV) return set_err(B200_ERR_NO_DEVICE, "device id >= 64");
+    HostPipe &g_pipe = g_pipes[dev];
+    std::lock_guard<std::mutex> lk(g_pipe.mu);
+    if (!g_pipe.ready) {
         for (int i = 0; i < HostPipe::NSLOT; ++i) {
             if ((rc = cuda_err(cudaStreamCreateWithFlags(&g_pipe.st[i], cudaStreamNonBlocking), "stream"))) return rc;
             if ((rc = cuda_err(cudaMalloc(&g_pipe.buf[i], 4 * HostPipe::CH * sizeof(double)), "cudaMalloc"))) return rc;
         }
-        g_pipe.dev = dev;
+        g_pipe.ready = true;
     }
     int64_t chunk = 0;
     for (int64_t off = 0; off < n; off += HostPipe::CH, ++chunk) {
