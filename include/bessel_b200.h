@@ -17,6 +17,19 @@
  *     Invalid arguments (n < 0, NULL pointer with n > 0) are rejected before
  *     any launch.  Out-of-domain inputs are NOT errors: they produce NaN in
  *     that element only (see each function).
+ *   - Alignment: 16-byte aligned arrays (any cudaMalloc / torch allocation)
+ *     move through the bulk-copy (TMA) engine; 8-byte aligned ones (e.g. a
+ *     view starting at an odd element) take a per-thread cp.async path with
+ *     identical results.
+ *   - Operating range: 1e-140 <= x <= 1e140, |v| <= 1e140 run on the fast
+ *     table-driven paths; finite arguments outside it are evaluated by the
+ *     same formulas with library functions and rescaling (slower, same
+ *     accuracy); IEEE special values follow each function's description.
+ *   - Thread safety: device entry points may be called concurrently from
+ *     several host threads and streams; host-buffer entry points serialise
+ *     per device on an internal pipeline (4 streams, 256 MB of staging).
+ *   - Determinism: results depend only on (v_i, x_i) -- not on n, the
+ *     position in the array, the stream or the alignment.
  */
 #ifndef BESSEL_B200_H
 #define BESSEL_B200_H
