@@ -249,6 +249,7 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
     constexpr int VEC = 16 / int(sizeof(T));          // elements per 16 bytes (bulk-copy granule)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t ntiles = (n + TILE - 1) / TILE;
+    fm_tables_init();
     auto tile_rem = [&](int64_t t) { return int(n - t * TILE < TILE ? n - t * TILE : TILE); };
 
     // stage tile t into buffer (t / gridDim.x) & 1

@@ -42,6 +42,21 @@ static __constant__ FmConst c_fm = {
     1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0,
 };
 
+#ifndef B200_SMEM_LOG
+#define B200_SMEM_LOG 1
+#endif
+#if B200_SMEM_LOG
+// {1/c_i, -log(1/c_i)} in shared memory (filled by fm_tables_init at kernel start)
+static __shared__ double2 s_logtab[1 << B200_LOG_TAB_BITS];
+__device__ __forceinline__ void fm_tables_init() {
+    for (int i = threadIdx.x; i < (1 << B200_LOG_TAB_BITS); i += blockDim.x)
+        s_logtab[i] = make_double2(g_logtab[i].invc, g_logtab[i].thi);
+    __syncthreads();
+}
+#else
+__device__ __forceinline__ void fm_tables_init() {}
+#endif
+
 // log(a) for finite normal a > 0.
 __device__ __forceinline__ double fm_log(double a) {
     const int hi = __double2hiint(a), lo = __double2loint(a);
@@ -49,8 +64,13 @@ __device__ __forceinline__ double fm_log(double a) {
     const int e = t >> 20;                                   // a = 2^e * m, m in [sqrt(1/2), sqrt(2))
     const int i = (t >> (20 - B200_LOG_TAB_BITS)) & ((1 << B200_LOG_TAB_BITS) - 1);
     const double m = __hiloint2double(hi - (e << 20), lo);
+#if B200_SMEM_LOG
+    const double2 c = s_logtab[i];
+    const double tlo = 0.0;
+#else
     const double2 c = __ldg(reinterpret_cast<const double2 *>(&g_logtab[i]));
     const double tlo = __ldg(&g_logtab[i].tlo);
+#endif
     const double r = fma(m, c.x, -1.0);                      // m / c_i - 1, |r| < 0.00195
     // log1p(r) - r = r^2 (-1/2 + r (1/3 + r (-1/4 + r (1/5 - r/6))))
     double p = fma(r, c_fm.log_c6, c_fm.log_c5);

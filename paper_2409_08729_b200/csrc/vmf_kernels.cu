@@ -110,6 +110,7 @@ constexpr int FIT_TPB = 256;
 __global__ void __launch_bounds__(FIT_TPB) vmf_fit_kernel(const double *__restrict__ colsum, int64_t n_total,
                                                           int64_t d, double *__restrict__ mu,
                                                           double *__restrict__ stats) {
+    fm_tables_init();
     __shared__ double s_red[FIT_TPB / 32];
     __shared__ double s_rbar;
     const double inv_n = 1.0 / double(n_total);
