@@ -37,6 +37,19 @@ template <> struct Tr<float> {
     __device__ static float rg(int i) { return c_rg_f[i]; }
 };
 
+// Constants used on every element of the mu / U paths.  In constant memory: a
+// double literal with a non-zero low word costs two UMOVs per use in SASS, a
+// __constant__ operand one LDCU (two per LDCU.128).
+enum : int { HC_INV2PI = 0, HC_PIO2, HC_LNPI, HC_ETA_HI, HC_ETA_BAND, HC_PI2, HC_N };
+static __constant__ double c_hot_d[HC_N] = {0.5 / CUDART_PI, CUDART_PI / 2.0, 1.1447298858494002,
+                                            B200_ETA_Z0_HI, 0.03, CUDART_PI * CUDART_PI};
+static __constant__ float c_hot_f[HC_N] = {float(0.5 / CUDART_PI), float(CUDART_PI / 2.0), 1.1447298858494002f,
+                                           B200_ETA_Z0_HI_F, 0.03f, float(CUDART_PI * CUDART_PI)};
+template <typename T>
+__device__ __forceinline__ T hc(int i) {
+    if constexpr (sizeof(T) == 8) return c_hot_d[i]; else return c_hot_f[i];
+}
+
 // 1/k for k = 1..400 (recurrences divide by the term index)
 #define B200_NINV 400
 static __constant__ double c_inv_d[B200_NINV + 1] = B200_INV_INIT;
@@ -146,7 +159,7 @@ __device__ __forceinline__ T log_bessel_mu(T v, T x) {
     if (!SAFE || x < Big<T>::v) {
         const T rx = fm_rcp(x);
         const T S = mu_series<T, IS_K>(v, rx);
-        const T c = IS_K ? T(CUDART_PI / 2.0) : T(0.5 / CUDART_PI);
+        const T c = IS_K ? hc<T>(HC_PIO2) : hc<T>(HC_INV2PI);
         return (IS_K ? -x : x) + T(0.5) * fm_log(S * S * rx * c);
     }
     const T S = mu_series<T, IS_K>(v, T(1) / x);
@@ -216,7 +229,7 @@ template <> struct EtaC<float> {
 template <typename T, bool SAFE>
 __device__ __forceinline__ T v_times_eta(T v, T x, T vs, T xs, T rhos, T rho) {
     // band test on z = x/v without a division: |x - z0 v| < 0.03 v
-    if (fabs(fma(-EtaC<T>::hi, v, x)) < T(0.03) * v) {
+    if (fabs(fma(-hc<T>(HC_ETA_HI), v, x)) < hc<T>(HC_ETA_BAND) * v) {
         const T rv = T(1) / v;
         const T z = x * rv;
         const T zlo = fma(-z, v, x) * rv;
@@ -267,7 +280,7 @@ __device__ __forceinline__ T log_bessel_u(T v, T x) {
     const T d = acc * w;                         // S - 1
     const T veta = v_times_eta<T, SAFE>(v, x, vs, xs, rhos, rho);
     // log S + 1/2 log(y_true c) with y_true = s y
-    const T c = IS_K ? T(CUDART_PI / 2.0) : T(0.5 / CUDART_PI);
+    const T c = IS_K ? hc<T>(HC_PIO2) : hc<T>(HC_INV2PI);
     const T tail = log1p_small<T, Log1pDeg<KU>::v>(d) + T(0.5) * (fm_log(y * c) + ls);
     return IS_K ? tail - veta : veta + tail;
 }
@@ -299,9 +312,9 @@ __device__ __forceinline__ void log_bessel_u_ik(T v, T x, T &li, T &lk) {
     const T veta = v_times_eta<T, false>(v, x, v, x, rho, rho);
     // log S_I = log1p(e + o), log S_K = log1p(e - o); one log of y for both:
     // 1/2 log(y pi/2) = 1/2 log(y/(2 pi)) + log(pi)
-    const T hl = T(0.5) * fm_log(y * T(0.5 / CUDART_PI));
+    const T hl = T(0.5) * fm_log(y * hc<T>(HC_INV2PI));
     li = veta + (hl + log1p_small<T, Log1pDeg<KU>::v>(e + o));
-    lk = (hl + T(1.1447298858494002)) + log1p_small<T, Log1pDeg<KU>::v>(e - o) - veta;
+    lk = (hl + hc<T>(HC_LNPI)) + log1p_small<T, Log1pDeg<KU>::v>(e - o) - veta;
 }
 
 template <typename T>
@@ -327,8 +340,8 @@ __device__ __forceinline__ void log_bessel_mu_ik(T v, T x, T &li, T &lk) {
         if (k >= 3 && fabs(term) <= Tr<T>::eps * T(0.25) * fabs(si)) break;
     }
     const T SI = fabs(si), SK = fabs(sk);
-    li = x + T(0.5) * fm_log(SI * SI * rx * T(0.5 / CUDART_PI));
-    lk = -x + T(0.5) * fm_log(SK * SK * rx * T(CUDART_PI / 2.0));
+    li = x + T(0.5) * fm_log(SI * SI * rx * hc<T>(HC_INV2PI));
+    lk = -x + T(0.5) * fm_log(SK * SK * rx * hc<T>(HC_PIO2));
 }
 
 // ---------------------------------------------------------------- series (I)
@@ -521,7 +534,7 @@ __device__ __forceinline__ T temme_kmu(T mu, T x, T &rho) {
 // Returns log K_mu and rho = K_{mu+1} / K_mu.  12-17 nodes on the band.
 template <typename T>
 __device__ __forceinline__ T trap_kmu(T mu, T x, T &rho) {
-    const T h = T(CUDART_PI * CUDART_PI) * fm_rcp(fma(T(0.8), x, T(42)));
+    const T h = hc<T>(HC_PI2) * fm_rcp(fma(T(0.8), x, T(42)));
     const T a = T(0.5) * h, a2 = a * a;
     // sinh(a) and 2 cosh(a) by their Taylor series (a <= 0.12: 5 terms exact to 2^-60)
     const T s1 = a * fma(a2 * T(1.0 / 6), fma(a2 * T(1.0 / 20), fma(a2 * T(1.0 / 42), fma(a2, T(1.0 / 72), T(1)), T(1)), T(1)), T(1));
