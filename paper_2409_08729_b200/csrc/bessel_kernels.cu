@@ -68,7 +68,7 @@ static int cuda_err(cudaError_t e, const char *where) {
 enum : int { FN_I = 0, FN_K = 1, FN_K_PAPER = 2, FN_IK = 3 };   // FN_IK: both, one pass
 
 // ------------------------------------------------------------------ binning
-// bins 0..6 = E_MU, E_U4, E_U6, E_U9, E_U13, fallback split by cost (series:
+// bins 0..6 = E_MU, E_UA, E_UB, E_UC, E_U13 (U by term count), fallback split by cost (series:
 // x <= 8 / x > 8; K: Temme series x <= 2 / trapezoid x > 2); 7 = the slow bin.
 // The fast evaluation paths (fastmath.cuh, SAFE = false) assume the operating
 // range 1e-140 <= x <= 1e140, |v| <= 1e140: there every intermediate (1/x,
@@ -114,9 +114,9 @@ __device__ __forceinline__ T eval_bin(int bin, T v, T x) {
     if (FN == FN_I) {
         switch (bin) {
             case E_MU: return log_bessel_mu<T, false, false>(v, x);
-            case E_U4: return log_bessel_u<T, false, 4, false>(v, x);
-            case E_U6: return log_bessel_u<T, false, 6, false>(v, x);
-            case E_U9: return log_bessel_u<T, false, 9, false>(v, x);
+            case E_UA: return log_bessel_u<T, false, KU_A, false>(v, x);
+            case E_UB: return log_bessel_u<T, false, KU_B, false>(v, x);
+            case E_UC: return log_bessel_u<T, false, KU_C, false>(v, x);
             case E_U13: return log_bessel_u<T, false, 13, false>(v, x);
             case E_FB_A:
             case E_FB_B: return log_iv_series<T, false>(v, x);
@@ -126,9 +126,9 @@ __device__ __forceinline__ T eval_bin(int bin, T v, T x) {
     const T av = fabs(v);
     switch (bin) {
         case E_MU: return log_bessel_mu<T, true, false>(av, x);
-        case E_U4: return log_bessel_u<T, true, 4, false>(av, x);
-        case E_U6: return log_bessel_u<T, true, 6, false>(av, x);
-        case E_U9: return log_bessel_u<T, true, 9, false>(av, x);
+        case E_UA: return log_bessel_u<T, true, KU_A, false>(av, x);
+        case E_UB: return log_bessel_u<T, true, KU_B, false>(av, x);
+        case E_UC: return log_bessel_u<T, true, KU_C, false>(av, x);
         case E_U13: return log_bessel_u<T, true, 13, false>(av, x);
         case E_FB_A:
         case E_FB_B: return FN == FN_K_PAPER ? log_kv_integral_paper<T>(av, x) : log_kv_fallback<T>(av, x);
@@ -144,9 +144,9 @@ __device__ __forceinline__ void eval_bin_ik(int bin, T v, T x, T &ri, T &rk) {
 #endif
     switch (bin) {
         case E_MU: log_bessel_mu_ik<T>(v, x, ri, rk); break;
-        case E_U4: log_bessel_u_ik<T, 4>(v, x, ri, rk); break;
-        case E_U6: log_bessel_u_ik<T, 6>(v, x, ri, rk); break;
-        case E_U9: log_bessel_u_ik<T, 9>(v, x, ri, rk); break;
+        case E_UA: log_bessel_u_ik<T, KU_A>(v, x, ri, rk); break;
+        case E_UB: log_bessel_u_ik<T, KU_B>(v, x, ri, rk); break;
+        case E_UC: log_bessel_u_ik<T, KU_C>(v, x, ri, rk); break;
         case E_U13: log_bessel_u_ik<T, 13>(v, x, ri, rk); break;
         case E_FB_A:
         case E_FB_B:

@@ -245,20 +245,14 @@ __device__ __forceinline__ T v_times_eta(T v, T x, T vs, T xs, T rhos, T rho) {
 
 // Number of U_K terms.  The paper's Table 1 fits regions for U4/U6/U9/U13 and
 // the GPU version keeps only U13 to avoid warp divergence (line 384).  With
-// the in-CTA binning divergence is gone, so all four come back, selected by an
-// a-priori truncation bound instead of the fitted regions (R12):
-// u_k(t) = t^k P_k(t^2) with sup_{t in [0,1]} |P_k| = P_k(0) =: M_k, and
-// w = t/v = 1/sqrt(v^2+x^2), so the first omitted term of U_K is at most
-// M_{K+1} w^{K+1} <= 2^-56 once sqrt(v^2+x^2) >= 1749 (K=4), 277 (K=6),
-// 77.6 (K=9).  Tested on max(v, x) <= sqrt(v^2+x^2) against 1800/280/80
-// (high words): conservative, never fewer terms than the bound allows.
-__device__ __forceinline__ int select_u_terms_hw(uint32_t hv, uint32_t hx) {
-    const uint32_t m = hv > hx ? hv : hx;
-    if (m >= B200_HW_R1800) return 4;
-    if (m >= B200_HW_R280) return 6;
-    if (m >= B200_HW_R80) return 9;
-    return 13;
-}
+// the in-CTA binning divergence is gone, so fewer terms come back where rho is
+// large, selected by an a-priori truncation bound instead of the fitted regions
+// (R12): u_k(t) = t^k P_k(t^2) with sup_{t in [0,1]} |P_k| = P_k(0) =:
+// M_k, and w = t/v = 1/sqrt(v^2+x^2), so the first omitted term of U_K is at
+// most M_{K+1} w^{K+1} <= 2^-56 once sqrt(v^2+x^2) >= rho_K (tables.h
+// B200_HW_RHO_K*: 277 for K=6, 107 for K=8, 61 for K=10).  Tested on
+// max(v, x) <= sqrt(v^2+x^2): conservative, never fewer terms than the bound
+// allows.  The bins (select_eval_hw) use K = KU_A/KU_B/KU_C/13.
 
 template <typename T, bool IS_K, int KU, bool SAFE>
 __device__ __forceinline__ T log_bessel_u(T v, T x) {
@@ -664,12 +658,29 @@ __device__ __forceinline__ T log_kv_integral_paper(T v, T x) {
 
 // ---------------------------------------------------------------- entry points
 // Evaluation sub-methods (bins): the region of Algorithm 1 refined by cost.
-enum : int { E_MU = 0, E_U4 = 1, E_U6 = 2, E_U9 = 3, E_U13 = 4, E_FB_A = 5, E_FB_B = 6 };
+// The U region splits into four bins by the number of terms K (R12): KU_A > ...
+// for large rho, 13 below; each bin's rho threshold is tables.h's bound for its K.
+#ifndef B200_KU_A
+#define B200_KU_A 6
+#endif
+#ifndef B200_KU_B
+#define B200_KU_B 8
+#endif
+#ifndef B200_KU_C
+#define B200_KU_C 10
+#endif
+#define B200_CAT_(a, b) a##b
+#define B200_CAT(a, b) B200_CAT_(a, b)
+#define B200_HW_RHO(K) B200_CAT(B200_HW_RHO_K, K)
+constexpr int KU_A = B200_KU_A, KU_B = B200_KU_B, KU_C = B200_KU_C;
+static_assert(KU_A < KU_B && KU_B < KU_C && KU_C < 13, "U bins: increasing term counts below 13");
+enum : int { E_MU = 0, E_UA = 1, E_UB = 2, E_UC = 3, E_U13 = 4, E_FB_A = 5, E_FB_B = 6 };
 
 __device__ __forceinline__ int select_eval_hw(double v, double x, uint32_t hv, uint32_t hx, uint32_t hw_split) {
     // selects, no nested branches: U sub-bin from max(v, x) (R12), fallback cost class from x
     const uint32_t m = hv > hx ? hv : hx;
-    const int eu = m >= B200_HW_R1800 ? E_U4 : m >= B200_HW_R280 ? E_U6 : m >= B200_HW_R80 ? E_U9 : E_U13;
+    const int eu = m >= B200_HW_RHO(B200_KU_A) ? E_UA : m >= B200_HW_RHO(B200_KU_B) ? E_UB
+                 : m >= B200_HW_RHO(B200_KU_C) ? E_UC : E_U13;
     const int ef = hx > hw_split ? E_FB_B : E_FB_A;
     const int e = is_u_hw(hv, hx) ? eu : ef;
     return is_mu_hw(v, x, hv, hx) ? E_MU : e;
@@ -682,9 +693,9 @@ template <typename T, bool SAFE>
 __device__ __forceinline__ T log_iv_eval(int e, T v, T x) {
     switch (e) {
         case E_MU: return log_bessel_mu<T, false, SAFE>(v, x);
-        case E_U4: return log_bessel_u<T, false, 4, SAFE>(v, x);
-        case E_U6: return log_bessel_u<T, false, 6, SAFE>(v, x);
-        case E_U9: return log_bessel_u<T, false, 9, SAFE>(v, x);
+        case E_UA: return log_bessel_u<T, false, KU_A, SAFE>(v, x);
+        case E_UB: return log_bessel_u<T, false, KU_B, SAFE>(v, x);
+        case E_UC: return log_bessel_u<T, false, KU_C, SAFE>(v, x);
         case E_U13: return log_bessel_u<T, false, 13, SAFE>(v, x);
         default: return log_iv_series<T, SAFE>(v, x);
     }
@@ -694,9 +705,9 @@ template <typename T, bool PAPER, bool SAFE>
 __device__ __forceinline__ T log_kv_eval(int e, T v, T x) {
     switch (e) {
         case E_MU: return log_bessel_mu<T, true, SAFE>(v, x);
-        case E_U4: return log_bessel_u<T, true, 4, SAFE>(v, x);
-        case E_U6: return log_bessel_u<T, true, 6, SAFE>(v, x);
-        case E_U9: return log_bessel_u<T, true, 9, SAFE>(v, x);
+        case E_UA: return log_bessel_u<T, true, KU_A, SAFE>(v, x);
+        case E_UB: return log_bessel_u<T, true, KU_B, SAFE>(v, x);
+        case E_UC: return log_bessel_u<T, true, KU_C, SAFE>(v, x);
         case E_U13: return log_bessel_u<T, true, 13, SAFE>(v, x);
         default: return PAPER ? log_kv_integral_paper<T>(v, x) : log_kv_fallback<T>(v, x);
     }

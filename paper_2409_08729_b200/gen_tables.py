@@ -129,9 +129,27 @@ def exp_table(n: int = EXP_TAB_N):
 # sharing C's high word (C' - C < 2^-20 C; reading R3).
 THRESHOLDS = {
     "X30": 30.0, "V15": 15.3919, "X59": 59.6925, "X19": 19.6931, "V07": 0.7, "V12": 12.6964,
-    "R1800": 1800.0, "R280": 280.0, "R80": 80.0, "X8": 8.0, "X2": 2.0, "X1E30": 1e30,
+    "X8": 8.0, "X2": 2.0, "X1E30": 1e30,
     "LO": 1e-140, "HI": 1e140,
 }
+
+
+def u_term_thresholds(kmin: int = 3, kmax: int = KMAX - 1, bits: int = 56):
+    """rho_K (integer, rounded up) from which K U-terms suffice (R12).
+
+    The first omitted term of the U_K sum is P_{K+1}(t^2) w^{K+1} with w = 1/rho,
+    rho = sqrt(v^2 + x^2) and |P_{K+1}| <= M_{K+1} := max over t^2 in [0, 1] (a
+    fine grid plus the endpoints; the maximum sits at t^2 = 0), so it is
+    <= 2^-bits once rho >= (M_{K+1} 2^bits)^(1/(K+1)).
+    """
+    import math
+    P = uk_P_coeffs(kmax + 1)
+    out = {}
+    for K in range(kmin, kmax + 1):
+        c = [float(a) for a in P[K + 1]]
+        M = max(abs(sum(cj * (i / 4096.0) ** j for j, cj in enumerate(c))) for i in range(4097))
+        out[K] = math.ceil((M * 2.0 ** bits) ** (1.0 / (K + 1)))
+    return out
 
 
 def hiword(c: float) -> int:
@@ -195,6 +213,10 @@ def render() -> str:
     lines.append("// dispatch thresholds: IEEE high words (gen_tables.THRESHOLDS)")
     for k, c in THRESHOLDS.items():
         lines.append("#define B200_HW_%s 0x%08Xu   // %r" % (k, hiword(c), c))
+    lines.append("// rho from which K U-terms leave a first omitted term <= 2^-56 (R12):")
+    lines.append("// B200_HW_RHO_K<K> = high word of that (integer) rho")
+    for K, r in u_term_thresholds().items():
+        lines.append("#define B200_HW_RHO_K%d 0x%08Xu   // %d" % (K, hiword(float(r)), r))
     lines.append("")
     hi, lo, ce = eta_root_taylor()
     lines.append("// eta(z) = sqrt(1+z^2) + log(z/(1+sqrt(1+z^2))): root z0 = HI + LO and")

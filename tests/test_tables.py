@@ -48,3 +48,18 @@ def test_generated_header_is_current():
     import os
     path = os.path.join(os.path.dirname(gen_tables.__file__), "csrc", "tables.h")
     assert open(path).read() == gen_tables.render()
+
+
+def test_u_term_thresholds_are_the_tightest_integers_of_the_bound():
+    # R12: rho_K is the smallest integer with M_{K+1} rho^-(K+1) <= 2^-56, where
+    # M_{K+1} = max |P_{K+1}| on [0, 1] attained at t^2 = 0 (checked here in exact arithmetic)
+    P = gen_tables.uk_P_coeffs(13)
+    th = gen_tables.u_term_thresholds()
+    for K, r in th.items():
+        c = P[K + 1]
+        M = abs(c[0])
+        grid = [sum(cj * Fraction(i, 64) ** j for j, cj in enumerate(c)) for i in range(65)]
+        assert max(abs(g) for g in grid) == M
+        assert M * Fraction(2) ** 56 <= Fraction(r) ** (K + 1)
+        assert M * Fraction(2) ** 56 > Fraction(r - 1) ** (K + 1)
+    assert (th[4], th[6], th[8], th[9], th[10]) == (1749, 277, 107, 78, 61)

@@ -12,8 +12,8 @@ import paper_2409_08729_b200 as B  # noqa: E402
 
 SETS = {
     "mu": ((0.0, 15.0), (30.0, 100.0)), "mu_far": ((0.0, 200.0), (1e3, 1e5)),
-    "u4": ((1800.0, 1e5), (1.0, 1e5)), "u6": ((280.0, 1800.0), (1.0, 1000.0)),
-    "u9": ((80.0, 280.0), (1.0, 200.0)), "u13": ((13.0, 80.0), (1.0, 60.0)),
+    "u6": ((280.0, 1e5), (1.0, 1e5)), "u8": ((107.0, 277.0), (1.0, 107.0)),
+    "u10": ((61.0, 107.0), (1.0, 60.0)), "u13": ((13.0, 61.0), (1.0, 60.0)),
     "u13_lowv": ((0.7, 13.0), (19.7, 30.0)), "fb_a": ((0.0, 12.69), (1e-3, 2.0)),
     "fb_b": ((0.0, 12.69), (2.0, 19.69)), "fb_b_lowv": ((0.0, 0.7), (2.0, 30.0)),
 }
@@ -47,6 +47,7 @@ def main(n=20000, seed=0):
 
 
 if __name__ == "__main__":
-    r = main()
+    # usage: python tools/accuracy_report.py [out.json] [points per set]
+    r = main(int(sys.argv[2])) if len(sys.argv) > 2 else main()
     if len(sys.argv) > 1:
         json.dump(r, open(sys.argv[1], "w"), indent=1)
