@@ -381,7 +381,7 @@ def run_ours(args):
                "h2d_bytes_per_step": 2 * ne * 8 * ws, "d2h_bytes_per_step": 2 * ne * 8 * ws,
                "note": "b200_log_ivkv_f64_host on pinned host arrays (every (n/e2e_pairs)-th pair of the "
                        "bench grid, all orders): v, x cross PCIe once per pair, both results come back; "
-                       "chunked H2D/kernel/D2H pipeline on 3 streams; host wall clock, max over ranks; "
+                       "chunked H2D/kernel/D2H pipeline on 4 streams (4M-pair chunks); host wall clock, max over ranks; "
                        "bytes and pairs are whole-job"}
         del vh, xh, oi, ok
 

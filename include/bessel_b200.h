@@ -27,7 +27,8 @@
  *     accuracy); IEEE special values follow each function's description.
  *   - Thread safety: device entry points may be called concurrently from
  *     several host threads and streams; host-buffer entry points serialise
- *     per device on an internal pipeline (4 streams, 256 MB of staging).
+ *     per device on an internal pipeline (4 streams, 512 MB of device
+ *     staging allocated on first use and kept for the process lifetime).
  *   - Determinism: results depend only on (v_i, x_i) -- not on n, the
  *     position in the array, the stream or the alignment.
  */

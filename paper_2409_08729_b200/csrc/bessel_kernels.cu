@@ -467,9 +467,19 @@ static int launch_eval(const T *v, const T *x, T *out, int64_t n, cudaStream_t s
 // Chunks of CH pairs cycle through NSLOT device slots, each with its own
 // stream: H2D(v,x) -> kernel -> D2H(out).  Copies of one slot overlap the
 // kernel of another and the two copy directions run on separate engines.
+#ifndef B200_HOST_NSLOT
+#define B200_HOST_NSLOT 4
+#endif
+#ifndef B200_HOST_CH_LOG2
+#define B200_HOST_CH_LOG2 22
+#endif
+
 struct HostPipe {
-    static constexpr int NSLOT = 4;
-    static constexpr int64_t CH = int64_t(1) << 21;   // 2M pairs per chunk (short pipeline fill)
+    static constexpr int NSLOT = B200_HOST_NSLOT;
+    // 4M pairs per chunk: measured against 0.5M-8M chunks, 3-8 slots, and a
+    // ramp of chunk sizes (tools/host_bench.py): larger copies win until the
+    // pipeline fill / drain dominates
+    static constexpr int64_t CH = int64_t(1) << B200_HOST_CH_LOG2;
     std::mutex mu;
     bool ready = false;
     cudaStream_t st[NSLOT] = {};
