@@ -395,3 +395,35 @@ def test_fused_deterministic_and_on_side_stream(B):
     s.synchronize()
     assert torch.equal(c[0], a[0]) and torch.equal(c[1], a[1])
     assert oracle.rel_err(ci.cpu().numpy(), oracle.log_iv(v, x)).max() <= TOL64
+
+
+@pytest.mark.timeout(600)
+def test_more_than_2_pow_31_pairs(B):
+    """n = 2^31 + 4097 pairs in one fused f64 call (69 GB of operands): element
+    and tile offsets past the 32-bit range.  Sampled outputs -- both sides of
+    2^31, the ragged last tile and random positions -- against the oracle, and
+    the same samples re-evaluated in a small call (results depend only on
+    (v_i, x_i), include/bessel_b200.h)."""
+    dev = torch.device("cuda:0")
+    n = 2 ** 31 + 4097
+    free, _ = torch.cuda.mem_get_info(dev)
+    if free < 4 * 8 * n + (8 << 30):
+        pytest.skip(f"needs {4 * 8 * n / 2**30:.0f} GiB free device memory")
+    g = torch.Generator(device=dev).manual_seed(11)
+    v = torch.empty(n, dtype=torch.float64, device=dev).uniform_(0.0, 60.0, generator=g)
+    x = torch.empty(n, dtype=torch.float64, device=dev).uniform_(1e-2, 120.0, generator=g)
+    oi, ok = B.log_ivkv(v, x)
+    torch.cuda.synchronize()
+    edge = torch.arange(-2048, 2048, device=dev) + 2 ** 31
+    tail = torch.arange(n - 2048, n, device=dev)
+    rnd = torch.randint(0, n, (4000,), generator=torch.Generator().manual_seed(5)).to(dev)
+    idx = torch.cat([edge, tail, rnd])
+    vs, xs = v[idx].clone(), x[idx].clone()
+    gi, gk = oi[idx].cpu().numpy(), ok[idx].cpu().numpy()
+    del v, x, oi, ok
+    torch.cuda.empty_cache()
+    si, sk = B.log_ivkv(vs, xs)
+    assert np.array_equal(si.cpu().numpy(), gi) and np.array_equal(sk.cpu().numpy(), gk)
+    vn, xn = vs.cpu().numpy(), xs.cpu().numpy()
+    assert oracle.rel_err(gi, oracle.log_iv(vn, xn)).max() <= TOL64
+    assert oracle.rel_err(gk, oracle.log_kv(vn, xn)).max() <= TOL64
