@@ -80,13 +80,31 @@ __global__ void __launch_bounds__(CS_TPB) colsum_partial_kernel(const T *__restr
     }
 }
 
-// Stage 2: colsum[j] (+)= sum_s part[s*d + j], slabs in fixed order.
-__global__ void colsum_reduce_kernel(const double *__restrict__ part, int64_t nslab, int64_t d,
-                                     double *__restrict__ colsum, int accumulate) {
-    for (int64_t j = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; j < d; j += int64_t(gridDim.x) * blockDim.x) {
+// Stage 2: colsum[j] (+)= sum_s part[s*d + j] in a fixed order: warp w of a
+// CTA sums slabs w, w + 8, w + 16, ... of 32 consecutive columns (one 256-byte
+// row segment per load), then the 8 warp partials are added in warp order --
+// deterministic for a given slab count, and d/32 CTAs instead of d/256 keep
+// enough loads in flight for the small-d case.
+constexpr int CR_WARPS = 8;
+__global__ void __launch_bounds__(32 * CR_WARPS) colsum_reduce_kernel(const double *__restrict__ part, int64_t nslab,
+                                                                     int64_t d, double *__restrict__ colsum,
+                                                                     int accumulate) {
+    __shared__ double sh[CR_WARPS][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int64_t c0 = int64_t(blockIdx.x) * 32; c0 < d; c0 += int64_t(gridDim.x) * 32) {
+        const int64_t j = c0 + lane;
         double s = 0.0;
-        for (int64_t k = 0; k < nslab; ++k) s += part[k * d + j];
-        colsum[j] = accumulate ? colsum[j] + s : s;
+        if (j < d)
+            for (int64_t k = w; k < nslab; k += CR_WARPS) s += part[k * d + j];
+        sh[w][lane] = s;
+        __syncthreads();
+        if (w == 0 && j < d) {
+            double t = sh[0][lane];
+#pragma unroll
+            for (int q = 1; q < CR_WARPS; ++q) t += sh[q][lane];
+            colsum[j] = accumulate ? colsum[j] + t : t;
+        }
+        __syncthreads();
     }
 }
 
@@ -243,8 +261,8 @@ static int colsum_impl(const T *X, int64_t n, int64_t d, int64_t ld, double *col
         colsum_partial_kernel<T, true><<<grid, CS_TPB, 0, s>>>(X, n, d, ld, rows_per, part);
     else
         colsum_partial_kernel<T, false><<<grid, CS_TPB, 0, s>>>(X, n, d, ld, rows_per, part);
-    const int64_t rb = (d + 255) / 256;
-    colsum_reduce_kernel<<<unsigned(rb < 4096 ? rb : 4096), 256, 0, s>>>(part, nslab, d, colsum, accumulate);
+    const int64_t rb = (d + 31) / 32;
+    colsum_reduce_kernel<<<unsigned(rb < 4096 ? rb : 4096), 32 * CR_WARPS, 0, s>>>(part, nslab, d, colsum, accumulate);
     g_launches.fetch_add(2, std::memory_order_relaxed);
     return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ERR_CUDA;
 }
