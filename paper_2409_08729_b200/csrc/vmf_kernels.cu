@@ -111,15 +111,26 @@ __global__ void __launch_bounds__(32 * CR_WARPS) colsum_reduce_kernel(const doub
 // ---------------------------------------------------------------- scalar part
 __device__ double log_iv_scalar(double v, double x) { return log_iv_scalar_eval<double>(v, x); }
 
-// A_p(kappa) = I_{p/2}(kappa) / I_{p/2-1}(kappa)  (line 677)
-__device__ double a_p(double p, double kappa) {
-    if (kappa <= 0.0) return 0.0;
-    return exp(log_iv_scalar(0.5 * p, kappa) - log_iv_scalar(0.5 * p - 1.0, kappa));
+// A_p(kappa) = I_{p/2}(kappa) / I_{p/2-1}(kappa)  (line 677).  Called by the
+// 64 threads of warps 0 and 1 with the same arguments: lane 0 of warp w
+// evaluates log I_{p/2 - w}(kappa), the two logs meet in shared memory behind
+// a named barrier over the two warps, so the two evaluations run concurrently.
+// lil = log I_{p/2-1}(kappa) (the log-likelihood needs it).
+__device__ double a_p(double p, double kappa, double *s_l, double &lil) {
+    const int w = threadIdx.x >> 5;
+    if (kappa <= 0.0) { lil = 0.0; return 0.0; }
+    if ((threadIdx.x & 31) == 0) s_l[w] = log_iv_scalar(0.5 * p - double(w), kappa);
+    asm volatile("bar.sync 1, 64;" ::: "memory");
+    const double l0 = s_l[0];
+    lil = s_l[1];
+    asm volatile("bar.sync 1, 64;" ::: "memory");   // s_l is rewritten by the next call
+    return exp(l0 - lil);
 }
 
 // F(kappa) of Eq. (kappa estimates)
-__device__ double newton_F(double p, double rbar, double k) {
-    const double A = a_p(p, k);
+__device__ double newton_F(double p, double rbar, double k, double *s_l) {
+    double lil;
+    const double A = a_p(p, k, s_l, lil);
     return k - (A - rbar) / (1.0 - A * A - (p - 1.0) / k * A);
 }
 
@@ -131,6 +142,7 @@ __global__ void __launch_bounds__(FIT_TPB) vmf_fit_kernel(const double *__restri
     fm_tables_init();
     __shared__ double s_red[FIT_TPB / 32];
     __shared__ double s_rbar;
+    __shared__ double s_l[2];
     const double inv_n = 1.0 / double(n_total);
     double loc = 0.0;
     for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
@@ -151,21 +163,27 @@ __global__ void __launch_bounds__(FIT_TPB) vmf_fit_kernel(const double *__restri
     __syncthreads();
     const double rbar = s_rbar;
     for (int64_t j = threadIdx.x; j < d; j += blockDim.x) mu[j] = colsum[j] * inv_n / rbar;
-    if (threadIdx.x != 0) return;
+    // the scalar part: warps 0 and 1 run it redundantly (identical control
+    // flow), lane 0 of each evaluates one of the two logs per A_p; thread 0 writes
+    if (threadIdx.x >= 64) return;
+    const bool w0 = threadIdx.x == 0;
 
     const double p = double(d);
-    stats[0] = rbar;
+    if (w0) stats[0] = rbar;
     if (!(rbar > 0.0 && rbar < 1.0)) {
-        for (int i = 1; i < 8; ++i) stats[i] = CUDART_NAN;
+        if (w0)
+            for (int i = 1; i < 8; ++i) stats[i] = CUDART_NAN;
         return;
     }
     // Eq. (kappa estimates)
     const double k0 = rbar * (p - rbar * rbar) / (1.0 - rbar * rbar);
-    const double k1 = newton_F(p, rbar, k0);
-    const double k2 = newton_F(p, rbar, k1);
-    stats[1] = k0;
-    stats[2] = k1;
-    stats[3] = k2;
+    const double k1 = newton_F(p, rbar, k0, s_l);
+    const double k2 = newton_F(p, rbar, k1, s_l);
+    if (w0) {
+        stats[1] = k0;
+        stats[2] = k1;
+        stats[3] = k2;
+    }
     // MLE: d logLik/dkappa = Rbar - A_p(kappa) (A_p strictly increasing), so
     // the maximiser is the root; safeguarded Newton from kappa2 with a
     // bracket [lo, hi] (lo: A < Rbar, hi: A > Rbar), bisection fallback.
@@ -173,7 +191,8 @@ __global__ void __launch_bounds__(FIT_TPB) vmf_fit_kernel(const double *__restri
     double k = (k2 > 0.0 && isfinite(k2)) ? k2 : k0;
     int it = 0;
     for (; it < 100; ++it) {
-        const double A = a_p(p, k);
+        double lil;
+        const double A = a_p(p, k, s_l, lil);
         const double g = A - rbar;
         if (g == 0.0) break;
         if (g < 0.0) lo = k; else hi = k;
@@ -185,11 +204,14 @@ __global__ void __launch_bounds__(FIT_TPB) vmf_fit_kernel(const double *__restri
         if (step <= 4e-16 * k) { ++it; break; }
         if (isfinite(hi) && (hi - lo) <= 4e-16 * hi) { ++it; break; }
     }
-    const double A = a_p(p, k);
-    stats[4] = k;
-    stats[5] = (0.5 * p - 1.0) * log(k) - 0.5 * p * log(2.0 * CUDART_PI) - log_iv_scalar(0.5 * p - 1.0, k) + k * rbar;
-    stats[6] = A - rbar;
-    stats[7] = double(it);
+    double lil;
+    const double A = a_p(p, k, s_l, lil);
+    if (w0) {
+        stats[4] = k;
+        stats[5] = (0.5 * p - 1.0) * log(k) - 0.5 * p * log(2.0 * CUDART_PI) - lil + k * rbar;
+        stats[6] = A - rbar;
+        stats[7] = double(it);
+    }
 }
 
 // ---------------------------------------------------------------- scratch
