@@ -57,8 +57,13 @@ def a_p(p, kappa):
         return 0.0
     h1, l1 = log_iv(p / 2.0, kappa, with_lo=True)
     h0, l0 = log_iv(p / 2.0 - 1.0, kappa, with_lo=True)
-    d = (float(h1) - float(h0)) + (float(l1) - float(l0))
+    d = (_scalar(h1) - _scalar(h0)) + (_scalar(l1) - _scalar(l0))
     return math.exp(d)
+
+
+def _scalar(a):
+    """The one element of a length-1 result array (marshalling only)."""
+    return float(np.asarray(a).reshape(-1)[0])
 
 
 def newton_F(p, rbar, kappa):
@@ -79,7 +84,7 @@ def kappa_estimates(p, rbar):
 
 def log_likelihood(p, rbar, kappa):
     """Mean log-likelihood (lines 685-689) with mean(mu^T x_i) = Rbar."""
-    lI = float(log_iv(p / 2.0 - 1.0, kappa))
+    lI = _scalar(log_iv(p / 2.0 - 1.0, kappa))
     return (p / 2.0 - 1.0) * math.log(kappa) - (p / 2.0) * math.log(2.0 * math.pi) - lI + kappa * rbar
 
 
