@@ -148,8 +148,12 @@ __device__ __forceinline__ void eval_bin_ik(int bin, T v, T x, T &ri, T &rk) {
         case E_UB: log_bessel_u_ik<T, KU_B>(v, x, ri, rk); break;
         case E_UC: log_bessel_u_ik<T, KU_C>(v, x, ri, rk); break;
         case E_U13: log_bessel_u_ik<T, 13>(v, x, ri, rk); break;
+        case E_FB_B:   // 2 < x <= 30
+#ifndef B200_IK_SERIES   // experiment switch: the power series for I on this band too
+            log_ivkv_trap<T>(v, x, ri, rk);   // I from the K values (Wronskian + Miller ratio)
+            break;
+#endif
         case E_FB_A:
-        case E_FB_B:
             ri = log_iv_series<T, false>(v, x);
             rk = log_kv_fallback<T>(v, x);
             break;

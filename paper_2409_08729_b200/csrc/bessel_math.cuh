@@ -617,6 +617,47 @@ __device__ __forceinline__ T log_kv_fallback(T v, T x) {
     return lk + T(fm_log(kp) + double(e2) * 0.6931471805599453);
 }
 
+// Fused fallback for 2 < x <= 30, v <= 12.7 (FN_IK): log K_v as in
+// log_kv_fallback, and log I_v from the same K values by the Wronskian
+//   I_v K_{v+1} + I_{v+1} K_v = 1/x   (DLMF 10.28.2; PAPER.md line 120 uses it as a check)
+// => log I_v = -log(x (K_{v+1} + r K_v)),  r = I_{v+1} / I_v,
+// with every term positive (no cancellation).  r comes from Miller's backward
+// recurrence y_{nu-1} = (2 nu / x) y_nu + y_{nu+1} started at nu = v + M with
+// y = (1, 0): the minimal solution I dominates.  Truncation error of r on the
+// whole band (tools/miller_steps.py):
+//   f64: M = floor(min(12 + x, 20 + 0.55 x)) + 1 (15-37 steps of 3 ops), < 8.1e-19;
+//   f32: M = floor(min(6 + x, 12 + 0.5 x)) + 1, < 2.3e-10, |y| < 2e11.
+// It replaces the power series (up to ~45 terms of 5 ops, 1/Gamma(v+1), two logs).
+template <typename T>
+__device__ __forceinline__ void log_ivkv_trap(T v, T x, T &ri, T &rk) {
+    const int nl = int(floor(v + T(0.5)));
+    const T mu = v - T(nl);
+    const T tox = T(2) * fm_rcp(x);
+    T rho;
+    const T lk = trap_kmu<T>(mu, x, rho);
+    // kp = K_v / K_mu, kn = K_{v+1} / K_mu (one recurrence step past v)
+    T km = T(1), kp = rho, nu = mu;
+    for (int i = 1; i <= nl; ++i) {
+        nu += T(1);
+        const T kn = fma(nu * tox, kp, km);
+        km = kp;
+        kp = kn;
+    }
+    // after the loop: kp = K_{v+1}/K_mu, km = K_v/K_mu
+    const int M = sizeof(T) == 8 ? int(fmin(T(12) + x, fma(T(0.55), x, T(20)))) + 1
+                                 : int(fmin(T(6) + x, fma(T(0.5), x, T(12)))) + 1;
+    T y1 = T(0), y0 = T(1);                 // y_{v+k+1}, y_{v+k}
+#pragma unroll 2
+    for (int k = M; k >= 1; --k) {
+        const T y = fma((v + T(k)) * tox, y0, y1);
+        y1 = y0;
+        y0 = y;
+    }
+    // r = y1 / y0;  1 / (I_v K_mu) = x (K_{v+1} + r K_v) / K_mu
+    rk = nl == 0 ? lk : lk + fm_log(km);
+    ri = -lk - fm_log(x * fma(km, y1, kp * y0) * fm_rcp(y0));
+}
+
 // ---------------------------------------------------------------- paper K
 // The paper's own small-argument K method (kept for fidelity studies):
 // Eq. (log Kv integral) (lines 251-254), n = 8, beta = 2n/(2v+1),

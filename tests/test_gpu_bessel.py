@@ -251,7 +251,7 @@ def _run_ivkv(B, v, x, dtype=torch.float64):
 
 
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("case", ["config0", "ragged", "wide", "eta", "special"])
+@pytest.mark.parametrize("case", ["config0", "ragged", "wide", "eta", "fallback_band", "special"])
 def test_fused_ivkv_against_oracle(B, case):
     """b200_log_ivkv_f64: both functions in one pass, each within the f64 bar."""
     if case == "config0":
@@ -263,6 +263,14 @@ def test_fused_ivkv_against_oracle(B, case):
     elif case == "wide":
         v = workloads.log_uniform(30_000, 1e-3, 1e5, seed=32)
         x = workloads.log_uniform(30_000, 1e-3, 1e5, seed=33)
+    elif case == "fallback_band":
+        # 2 < x <= 30, v <= 12.7: the fused pass takes log I from the K values
+        # (Wronskian + Miller ratio); edges of the band included
+        rng = np.random.default_rng(37)
+        v = rng.uniform(0.0, 12.69, 20_000)
+        x = rng.uniform(2.0, 30.0, 20_000)
+        v[:8] = [0.0, 0.5, 0.4999, 12.69, 12.5, 1.0, 0.7, 0.0]
+        x[:8] = [2.000001, 30.0, 2.5, 2.000001, 19.69, 19.7, 29.99, 29.99]
     elif case == "eta":
         v = workloads.log_uniform(10_000, 50.0, 1e5, seed=34)
         x = v * 0.66274341934918158 * (1 + np.random.default_rng(35).uniform(-0.1, 0.1, v.size))

@@ -63,7 +63,7 @@ def test_fit_against_oracle(B, d, rbar):
     def cond_tol(k_at, step, kref):
         A = ovmf.a_p(d, k_at)
         dA = abs(1 - A * A - (d - 1) / k_at * A)
-        delta = 64 * eps * max(abs(float(oracle.log_iv(d / 2, k_at))), 1.0)
+        delta = 64 * eps * max(abs(float(oracle.log_iv(d / 2, k_at)[0])), 1.0)
         return 1e-12 * kref + (A + abs(step) * (2 * A + (d - 1) / k_at)) * A * delta / dA
 
     prev = ref["kappa0"]
