@@ -153,7 +153,15 @@ __device__ __forceinline__ void eval_bin_ik(int bin, T v, T x, T &ri, T &rk) {
             log_ivkv_trap<T>(v, x, ri, rk);   // I from the K values (Wronskian + Miller ratio)
             break;
 #endif
-        case E_FB_A:
+        case E_FB_A:   // x <= 2
+#ifndef B200_IK_SERIES_A
+            if constexpr (sizeof(T) == 8) {
+                if (x >= T(1e-6) && x <= T(2)) {
+                    log_ivkv_trap<T, true>(v, x, ri, rk);   // Temme K values, Wronskian + Miller ratio
+                    break;
+                }
+            }
+#endif
             ri = log_iv_series<T, false>(v, x);
             rk = log_kv_fallback<T>(v, x);
             break;

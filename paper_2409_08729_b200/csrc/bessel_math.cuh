@@ -628,13 +628,16 @@ __device__ __forceinline__ T log_kv_fallback(T v, T x) {
 //   f64: M = floor(min(12 + x, 20 + 0.55 x)) + 1 (15-37 steps of 3 ops), < 8.1e-19;
 //   f32: M = floor(min(6 + x, 12 + 0.5 x)) + 1, < 2.3e-10, |y| < 2e11.
 // It replaces the power series (up to ~45 terms of 5 ops, 1/Gamma(v+1), two logs).
-template <typename T>
+// TEMME = true: the same on 1e-6 <= x <= 2 with K_mu, K_{mu+1} from Temme's
+// series (f64 only: there |y| < 4.1e98 and K_{v+1}/K_mu < 1e97, so neither
+// the recurrences nor x (K_{v+1} + r K_v) / K_mu leave the double range).
+template <typename T, bool TEMME = false>
 __device__ __forceinline__ void log_ivkv_trap(T v, T x, T &ri, T &rk) {
     const int nl = int(floor(v + T(0.5)));
     const T mu = v - T(nl);
     const T tox = T(2) * fm_rcp(x);
     T rho;
-    const T lk = trap_kmu<T>(mu, x, rho);
+    const T lk = TEMME ? temme_kmu<T>(mu, x, rho) : trap_kmu<T>(mu, x, rho);
     // kp = K_v / K_mu, kn = K_{v+1} / K_mu (one recurrence step past v)
     T km = T(1), kp = rho, nu = mu;
     for (int i = 1; i <= nl; ++i) {

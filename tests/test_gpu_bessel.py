@@ -251,7 +251,7 @@ def _run_ivkv(B, v, x, dtype=torch.float64):
 
 
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("case", ["config0", "ragged", "wide", "eta", "fallback_band", "special"])
+@pytest.mark.parametrize("case", ["config0", "ragged", "wide", "eta", "fallback_band", "temme_band", "special"])
 def test_fused_ivkv_against_oracle(B, case):
     """b200_log_ivkv_f64: both functions in one pass, each within the f64 bar."""
     if case == "config0":
@@ -271,6 +271,14 @@ def test_fused_ivkv_against_oracle(B, case):
         x = rng.uniform(2.0, 30.0, 20_000)
         v[:8] = [0.0, 0.5, 0.4999, 12.69, 12.5, 1.0, 0.7, 0.0]
         x[:8] = [2.000001, 30.0, 2.5, 2.000001, 19.69, 19.7, 29.99, 29.99]
+    elif case == "temme_band":
+        # x <= 2, v <= 12.7: for 1e-6 <= x the fused pass takes log I from
+        # Temme's K values (Wronskian + Miller ratio); below 1e-6 the series
+        rng = np.random.default_rng(38)
+        v = rng.uniform(0.0, 12.69, 20_000)
+        x = workloads.log_uniform(20_000, 1e-8, 2.0, seed=39)
+        v[:6] = [0.0, 0.5, 12.69, 12.69, 0.0, 7.3]
+        x[:6] = [1e-6, 2.0, 1e-6, 2.0, 0.999999e-6, 1.0000001e-6]
     elif case == "eta":
         v = workloads.log_uniform(10_000, 50.0, 1e5, seed=34)
         x = v * 0.66274341934918158 * (1 + np.random.default_rng(35).uniform(-0.1, 0.1, v.size))
