@@ -85,6 +85,10 @@ int b200_log_kv_f32(const float *v_d, const float *x_d, float *out_d, int64_t n,
  * are read once, classification / binning is shared, and inside the mu and U
  * regions the expansions share every term (I and K differ only by the sign
  * pattern (-1)^k, Eqs. (log Iv mu k)/(log Kv mu k), (log Iv u k)/(log Kv u k)).
+ * In the small-argument fallback region (1e-6 <= x <= 30 for f64, 2 < x <= 30
+ * for f32) log I is taken from the K values by the Wronskian
+ * I_v K_{v+1} + I_{v+1} K_v = 1/x with I_{v+1}/I_v from Miller's backward
+ * recurrence instead of the power series of Eq. (Iv infinite series).
  *   out_i_d[i] = log I_{v_i}(x_i), out_k_d[i] = log K_{v_i}(x_i), with the
  *   domains and special values of the two functions above (v < 0: out_i NaN,
  *   out_k = log K_{|v|}).  Results equal the separate calls to the stated
