@@ -63,3 +63,44 @@ def test_u_term_thresholds_are_the_tightest_integers_of_the_bound():
         assert M * Fraction(2) ** 56 <= Fraction(r) ** (K + 1)
         assert M * Fraction(2) ** 56 > Fraction(r - 1) ** (K + 1)
     assert (th[4], th[6], th[8], th[9], th[10]) == (1749, 277, 107, 78, 61)
+
+
+def test_miller_step_counts_in_kernel_source():
+    """The fused fallback's Miller start M(x) (bessel_math.cuh, log_ivkv_trap),
+    read from the kernel source, keeps the truncation error of r = I_{v+1}/I_v below
+    2^-60 (f64) / 2^-30 (f32) on the band 1e-6 <= x <= 30, v <= 12.7.  Reference r: the
+    same recurrence from M = 120 in long double, cross-checked against scipy's ive
+    ratio (an independent routine) to 1e-13."""
+    import os
+    import re
+
+    import numpy as np
+    import scipy.special as sps
+
+    src = open(os.path.join(os.path.dirname(gen_tables.__file__), "csrc", "bessel_math.cuh")).read()
+    num = r"T\(([\d.]+)\)"
+    m = re.search(r"const int M = sizeof\(T\) == 8 \? int\(fmin\(" + num + r" \+ x, fma\(" + num + r", x, " + num
+                  + r"\)\)\) \+ 1\s*: int\(fmin\(" + num + r" \+ x, fma\(" + num + r", x, " + num + r"\)\)\) \+ 1;", src)
+    assert m, "M(x) expression not found in log_ivkv_trap"
+    a64, b64, c64, a32, b32, c32 = (float(g) for g in m.groups())
+    L = np.longdouble
+
+    def ratio(v, x, M):
+        y1, y0 = L(0), L(1)
+        for k in range(M, 0, -1):
+            y1, y0 = y0, (2 * (L(v) + k) / L(x)) * y0 + y1
+            if y0 > 1e300:
+                y0, y1 = y0 * L(1e-300), y1 * L(1e-300)
+        return y1 / y0
+
+    xs = [1e-6, 1e-3, 0.3, 1.0, 2.0, 2.5, 4.9, 8.9, 13.0, 19.7, 25.0, 30.0]
+    for x in xs:
+        m64 = int(min(a64 + x, b64 * x + c64)) + 1
+        m32 = int(min(a32 + x, b32 * x + c32)) + 1
+        for v in (0.0, 0.5, 1.0, 4.2, 8.0, 12.69):
+            ref = ratio(v, x, 120)
+            if x >= 1e-3:
+                assert abs(float(ref) - sps.ive(v + 1, x) / sps.ive(v, x)) <= 1e-13 * float(ref)
+            assert float(abs(ratio(v, x, m64) - ref) / ref) < 2.0 ** -60, (x, v, m64)
+            if x > 2:
+                assert float(abs(ratio(v, x, m32) - ref) / ref) < 2.0 ** -30, (x, v, m32)
