@@ -650,9 +650,13 @@ __device__ __forceinline__ void log_ivkv_trap(T v, T x, T &ri, T &rk) {
     const int M = sizeof(T) == 8 ? int(fmin(T(12) + x, fma(T(0.55), x, T(20)))) + 1
                                  : int(fmin(T(6) + x, fma(T(0.5), x, T(12)))) + 1;
     T y1 = T(0), y0 = T(1);                 // y_{v+k+1}, y_{v+k}
+    // order counter nu = v + k kept in T: v + M rounds once, each nu - 1 is exact
+    // (nu < 64); an int -> T conversion per step (I2F.F64) cost 5% of this band
+    T nuk = v + T(M);
 #pragma unroll 2
     for (int k = M; k >= 1; --k) {
-        const T y = fma((v + T(k)) * tox, y0, y1);
+        const T y = fma(nuk * tox, y0, y1);
+        nuk -= T(1);
         y1 = y0;
         y0 = y;
     }
