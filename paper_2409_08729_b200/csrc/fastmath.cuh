@@ -77,12 +77,7 @@ __device__ __forceinline__ double fm_log(double a) {
     p = fma(p, r, -0.25);
     p = fma(p, r, c_fm.log_c3);
     p = fma(p, r, -0.5);
-#ifdef B200_LOG_MAGIC
-    // double(e) without I2F.F64: 2^52 + 2^31 + e from the bit pattern, minus the bias (one DADD)
-    const double ed = __hiloint2double(0x43300000, e ^ 0x80000000) - 4503601774854144.0;
-#else
-    const double ed = double(e);
-#endif
+    const double ed = double(e);   // I2F.F64 (a DADD-based magic-number conversion measured +1%: FP64 pipe)
     const double h = fma(ed, c_fm.ln2_hi, c.y);
     const double l = fma(ed, c_fm.ln2_lo, tlo);
     return h + (r + fma(r * r, p, l));
