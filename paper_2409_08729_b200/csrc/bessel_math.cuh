@@ -619,7 +619,8 @@ __device__ __forceinline__ T log_kv_fallback(T v, T x) {
 
 // Fused fallback for 2 < x <= 30, v <= 12.7 (FN_IK): log K_v as in
 // log_kv_fallback, and log I_v from the same K values by the Wronskian
-//   I_v K_{v+1} + I_{v+1} K_v = 1/x   (DLMF 10.28.2; PAPER.md line 120 uses it as a check)
+//   I_v K_{v+1} + I_{v+1} K_v = 1/x   (DLMF 10.28.2; not in PAPER.md, whose small-x I is the
+//   series of Eq. (Iv infinite series), line 127 -- a design choice of this implementation)
 // => log I_v = -log(x (K_{v+1} + r K_v)),  r = I_{v+1} / I_v,
 // with every term positive (no cancellation).  r comes from Miller's backward
 // recurrence y_{nu-1} = (2 nu / x) y_nu + y_{nu+1} started at nu = v + M with
