@@ -188,3 +188,62 @@ def test_vmf_mean_direction_and_gradient():
         fd = (vmf.log_likelihood(p, rbar, k + h) - vmf.log_likelihood(p, rbar, k - h)) / (2 * h)
         an = rbar - vmf.a_p(p, k)
         assert abs(fd - an) <= 1e-6 * max(1.0, abs(an)) + 1e-7
+
+
+def test_vmf_loglik_p3_closed_form():
+    """p = 3: I_{1/2}(k) = sqrt(2/(pi k)) sinh k, so C_3(k) = k / (4 pi sinh k) and the mean
+    log-likelihood of PAPER.md §6.3 (lines 685-689, density normaliser lines 666-668) is
+    log k - log(4 pi sinh k) + k Rbar.  Evaluated here at 50 digits with mpmath, independently
+    of the oracle's series: a slip in the (p/2 - 1) log k, the (p/2) log 2 pi or the
+    log I_{p/2-1} term fails it."""
+    for rbar in (0.05, 0.5, 0.93):
+        for k in (1e-3, 0.7, 3.0, 45.0, 600.0):
+            K = mpmath.mpf(k)
+            ref = mpmath.log(K) - mpmath.log(4 * mpmath.pi * mpmath.sinh(K)) + K * mpmath.mpf(rbar)
+            got = vmf.log_likelihood(3, rbar, k)
+            assert abs(got - float(ref)) <= 4e-15 * max(1.0, abs(float(ref))), (rbar, k, got, float(ref))
+
+
+@pytest.mark.parametrize("p", [3, 64, 2048, 32768])
+def test_vmf_loglik_uniform_limit(p):
+    """kappa -> 0: f_p -> the uniform density on S^{p-1}, 1 / |S^{p-1}| = Gamma(p/2) / (2 pi^{p/2})
+    (PAPER.md lines 666-668 with I_{p/2-1}(k) ~ (k/2)^{p/2-1} / Gamma(p/2)); p = 3 gives -log 4 pi."""
+    k = 1e-9
+    ref = math.lgamma(p / 2.0) - math.log(2.0) - (p / 2.0) * math.log(math.pi)
+    got = vmf.log_likelihood(p, 0.3, k)          # k Rbar = 3e-10 and O(k^2) terms: below 1e-9
+    assert abs(got - ref) <= 1e-9 * max(1.0, abs(ref)), (p, got, ref)
+    if p == 3:
+        assert abs(ref + math.log(4 * math.pi)) < 1e-15
+
+
+# ------------------------------------------------------------- the parity yardstick
+def test_rel_err_definition():
+    """oracle.rel_err (DESIGN.md R1): |got - ref| / max(|ref|, 1); NaN anywhere -> inf;
+    infinities must match in sign; finite vs infinite -> inf."""
+    inf, nan = np.inf, np.nan
+    got = np.array([1.0, 0.0, 0.5 + 1e-14, 100.0 + 1e-11, -3.0, inf, -inf, inf, 2.0, nan, 1.0, inf, 0.0])
+    ref = np.array([1.0, 0.0, 0.5, 100.0, 3.0, inf, -inf, -inf, inf, 1.0, nan, 7.0, 1e-300])
+    e = oracle.rel_err(got, ref)
+    assert e[0] == 0.0 and e[1] == 0.0                             # exact
+    assert abs(e[2] - 1e-14) < 1e-17                               # |ref| < 1: absolute (the floor)
+    assert abs(e[3] - 1e-13) < 1e-16                               # |ref| >= 1: relative
+    assert e[4] == 2.0                                             # sign error
+    assert e[5] == 0.0 and e[6] == 0.0                             # same infinities
+    assert np.all(np.isinf(e[7:12]))                               # opposite infinities, inf vs finite, NaN
+    assert e[12] == 1e-300
+    assert oracle.rel_err(np.array([]), np.array([])).size == 0
+    assert np.all(e >= 0)
+
+
+def test_mean_resultant_rows_matches_fsum():
+    """mean_resultant_rows (numpy pairwise column sums, used for the full-size GPU test) against
+    mean_direction's math.fsum column sums (exact rounding), to 1e-15."""
+    rng = np.random.default_rng(7)
+    for n, d, c in ((500, 33, 0.4), (20000, 64, 0.05), (3, 2048, 1.0)):
+        X = rng.normal(size=(n, d)) / math.sqrt(d)
+        X[:, 0] += c
+        X /= np.linalg.norm(X, axis=1, keepdims=True)
+        _, rbar, _ = vmf.mean_direction(X)
+        assert abs(vmf.mean_resultant_rows(X) - rbar) <= 1e-15, (n, d)
+        assert abs(vmf.mean_resultant_rows(X.astype(np.float32)) -
+                   vmf.mean_direction(X.astype(np.float32).astype(np.float64))[1]) <= 1e-15
