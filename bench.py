@@ -9,8 +9,11 @@ same work as two calls (b200_log_iv_f64 then b200_log_kv_f64) is timed beside
 it and reported as "separate_calls".  Inputs (3.5 GB) and outputs (3.5 GB)
 live in HBM, far larger than L2.
 
-Multi-GPU: one process per GPU (torchrun), every rank evaluates its own
-220M-pair batch (weak scaling, no data-path collective); time = max over ranks.
+Multi-GPU: one process per GPU.  `--gpus N` without torchrun re-launches the
+command under torch.distributed.run (N ranks); under torchrun WORLD_SIZE must
+equal N.  Every rank evaluates its own 220M-pair batch (weak scaling, no
+data-path collective); time = max over ranks.  extra.bench_grid_strong splits
+ONE 220M-pair grid contiguously over the ranks (strong scaling).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
@@ -212,6 +215,21 @@ def run_extra(args, B, workloads, ws, rank, dev, stream, dist):
     import torch
     from paper_2409_08729_b200.parallel import shard_range
     out = {}
+    # -- strong scaling of the headline: ONE global bench grid (11 x n_per_v pairs) split
+    #    contiguously over the ranks (parallel.shard_range), no collective on the data path
+    ntot = N_ORDERS * args.n_per_v
+    g0, g1 = shard_range(ntot, ws, rank)
+    gv, gx = workloads.bench_grid_slice(args.n_per_v, g0, g1, seed=0, device=dev)
+    gi, gk = torch.empty_like(gv), torch.empty_like(gv)
+    B.log_ivkv(gv, gx, gi, gk)
+    reps = 3
+    ms = _timed(lambda: B.log_ivkv(gv, gx, gi, gk), reps, stream, dist)
+    out["bench_grid_strong"] = {
+        "config": f"one global bench grid of {ntot} pairs (v in {{2^0..2^10}} x {args.n_per_v} x~U[1,100]) "
+                  f"split contiguously over {ws} GPU(s): rank {rank} holds [{g0}, {g1})",
+        "value": 2 * ntot * reps / (ms / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ms / reps,
+        "scaling": "strong", "time": "CUDA events, max over ranks"}
+    del gv, gx, gi, gk
     # -- configs[3]: v in {0} U logspace(1e-3,1e5) x x in logspace(1e-3,1e5), 16384^2 pairs
     nv = nx = 16384
     r0, r1 = shard_range(nv, ws, rank)
@@ -269,22 +287,24 @@ def run_extra(args, B, workloads, ws, rank, dev, stream, dist):
     hbm_peak, _ = _peaks()
     vm = {}
     for d in (2048, 8192, 32768):
-        X, _ = workloads.vmf_features(hi - lo, d, rbar=0.15, seed=100 + rank, device=dev)
+        # rows [lo, hi) of ONE 50000 x d matrix (mu and every row independent of the world size)
+        X, _ = workloads.vmf_features(n, d, rbar=0.15, seed=100, device=dev, rows=(lo, hi))
         pg = dist.group.WORLD if dist else None
         mu, st = B.vmf_fit(X, process_group=pg)
         torch.cuda.synchronize()
         reps = 5
         ms = _timed(lambda: B.vmf_fit(X, process_group=pg), reps, stream, dist)
-        cs = torch.empty(d, dtype=torch.float64, device=dev)
-        ms_cs = _timed(lambda: B.vmf_colsum(X, out=cs), reps, stream, None)
+        cs = torch.empty(d + 1, dtype=torch.float64, device=dev)
+        ms_cs = _timed(lambda: B.vmf_colsum(X, out=cs, with_count=True), reps, stream, None)
         gbs = (hi - lo) * d * 4 / (ms_cs / reps / 1e3) / 1e9
         vm[str(d)] = {"ms_per_fit": ms / reps, "colsum_ms": ms_cs / reps,
                       "colsum_roofline": {"bound": "hbm", "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
                                           "frac": gbs / hbm_peak},
                       "rbar": float(st[0].item()), "kappa_mle": float(st[4].item())}
         del X
-    out["vmf_fit"] = {"config": f"BASELINE configs[4]: {n} x d unit-norm f32 features (Rbar 0.15), rows sharded "
-                                f"over {ws} GPU(s), one all-reduce of the d-vector", "per_d": vm}
+    out["vmf_fit"] = {"config": f"BASELINE configs[4]: one {n} x d unit-norm f32 feature matrix (Rbar 0.15), "
+                                f"rows sharded over {ws} GPU(s), one all-reduce of d + 1 doubles (column sums "
+                                "and the row count)", "per_d": vm}
     return out
 
 
@@ -460,6 +480,24 @@ def main():
     ap.add_argument("--skip-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     args = ap.parse_args()
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    ws_env = os.environ.get("WORLD_SIZE")
+    if ws_env is None and args.gpus > 1:
+        # one process per GPU: re-launch this command under torch.distributed.run
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.stdout.flush()
+        os.execv(sys.executable, cmd)
+    if ws_env is not None and int(ws_env) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws_env} (launch one process per GPU, "
+              "or omit torchrun and let --gpus spawn them)", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args)
     else:

@@ -21,10 +21,12 @@
  *     move through the bulk-copy (TMA) engine; 8-byte aligned ones (e.g. a
  *     view starting at an odd element) take a per-thread cp.async path with
  *     identical results.
- *   - Operating range: 1e-140 <= x <= 1e140, |v| <= 1e140 run on the fast
- *     table-driven paths; finite arguments outside it are evaluated by the
- *     same formulas with library functions and rescaling (slower, same
- *     accuracy); IEEE special values follow each function's description.
+ *   - Operating range: 1e-140 <= x <= 1e140, |v| <= 1e140 (f64) and
+ *     1e-18 <= x <= 1e18, |v| <= 1e18 (f32) run on the fast table-driven
+ *     paths; finite arguments outside it (subnormals included) are evaluated
+ *     by the same formulas with library functions, rescaling and scaled
+ *     recurrences (slower, same accuracy); IEEE special values follow each
+ *     function's description.
  *   - Thread safety: device entry points may be called concurrently from
  *     several host threads and streams; host-buffer entry points serialise
  *     per device on an internal pipeline (4 streams, 512 MB of device
@@ -123,8 +125,14 @@ int b200_log_ivkv_f64_host(const double *v_h, const double *x_h, double *out_i_h
  * b200_vmf_colsum_*: colsum_d[j] (+)= sum_i X[i, j] over the n rows of the
  *   row-major n x d matrix X_d (leading dimension ld >= d elements), fp64
  *   accumulation.  If accumulate == 0 colsum_d is overwritten, else added to.
- *   This is the data-parallel part (Eq. (mean direction estimate), line 672);
- *   with rows sharded over GPUs the caller all-reduces colsum_d.
+ *   This is the data-parallel part (Eq. (mean direction estimate), line 672).
+ *   with_count != 0: colsum_d holds d + 1 doubles and colsum_d[d] (+)= n, so
+ *   with rows sharded over GPUs ONE all-reduce of the d + 1 doubles carries
+ *   both the column sums and the global row count.  Deterministic for a given
+ *   (n, d, device).  Scratch: the per-slab partials use a library-owned device
+ *   buffer per (device, stream), grown on demand and kept for the process;
+ *   concurrent calls on different streams or host threads are safe.
+ *   Errors: n < 0, d < 0, ld < d, NULL X with n > 0, NULL colsum_d.
  *
  * b200_vmf_fit_from_colsum: given the global column sum (d doubles) and the
  *   global row count n_total, computes on the device
@@ -136,14 +144,16 @@ int b200_log_ivkv_f64_host(const double *v_h, const double *x_h, double *out_i_h
  *     stats_d[5]   = logLik(kappa_mle)                 (lines 685-689)
  *     stats_d[6]   = A_p(kappa_mle) - Rbar  (stationarity residual)
  *     stats_d[7]   = number of MLE iterations
- *   stats_d must hold 8 doubles.  p = d.  Rbar outside (0,1) -> stats NaN.
+ *   stats_d must hold 8 doubles.  p = d.  n_total == 0: the row count is read
+ *   from colsum_d[d] (a with_count column sum).  Rbar outside (0,1) -> stats NaN.
+ *   Errors: d < 2, n_total < 0, NULL pointers.
  *
- * b200_vmf_fit_*: both steps on one device (workspace: d doubles, device).
+ * b200_vmf_fit_*: both steps on one device (workspace: d doubles, device); n >= 1.
  */
 int b200_vmf_colsum_f32(const float *X_d, int64_t n, int64_t d, int64_t ld, double *colsum_d,
-                        int accumulate, void *stream);
+                        int accumulate, int with_count, void *stream);
 int b200_vmf_colsum_f64(const double *X_d, int64_t n, int64_t d, int64_t ld, double *colsum_d,
-                        int accumulate, void *stream);
+                        int accumulate, int with_count, void *stream);
 int b200_vmf_fit_from_colsum(const double *colsum_d, int64_t n_total, int64_t d, double *mu_d,
                              double *stats_d, void *stream);
 int b200_vmf_fit_f32(const float *X_d, int64_t n, int64_t d, double *workspace_d, double *mu_d,

@@ -102,23 +102,48 @@ def classify(v: torch.Tensor, x: torch.Tensor) -> torch.Tensor:
     return m
 
 
-def _host_call(name, v, x, out):
-    v = np.ascontiguousarray(v, dtype=np.float64) if not isinstance(v, torch.Tensor) else v
-    x = np.ascontiguousarray(x, dtype=np.float64) if not isinstance(x, torch.Tensor) else x
-    if isinstance(v, torch.Tensor):
+def _host_arrays(v, x):
+    """Host float64 inputs (CPU torch tensors or array-likes), contiguous, same shape."""
+    if isinstance(v, torch.Tensor) or isinstance(x, torch.Tensor):
+        if not (isinstance(v, torch.Tensor) and isinstance(x, torch.Tensor)):
+            raise TypeError("host variants take two CPU tensors or two numpy arrays")
         if v.is_cuda or x.is_cuda or v.dtype != torch.float64 or x.dtype != torch.float64:
             raise TypeError("host variants take float64 CPU tensors or numpy arrays")
         v, x = v.contiguous(), x.contiguous()
-        if out is None:
-            out = torch.empty_like(v, pin_memory=v.is_pinned())
-        pv, px, po, n = v.data_ptr(), x.data_ptr(), out.data_ptr(), v.numel()
     else:
-        if out is None:
-            out = np.empty_like(v)
-        pv, px, po, n = v.ctypes.data, x.ctypes.data, out.ctypes.data, v.size
-    if (v.shape if hasattr(v, "shape") else None) != (x.shape if hasattr(x, "shape") else None):
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+    if tuple(v.shape) != tuple(x.shape):
         raise ValueError("v and x must have the same shape")
-    check(getattr(lib(), name)(pv, px, po, n), name)
+    return v, x
+
+
+def _host_out(v, out):
+    """A host float64 output like v (allocated if None; checked otherwise: the C call writes n doubles)."""
+    if isinstance(v, torch.Tensor):
+        if out is None:
+            return torch.empty_like(v, pin_memory=v.is_pinned()), None
+        if not isinstance(out, torch.Tensor) or out.is_cuda or out.dtype != torch.float64 \
+                or tuple(out.shape) != tuple(v.shape) or not out.is_contiguous():
+            raise ValueError("out must be a contiguous float64 CPU tensor shaped like v")
+        return out, None
+    if out is None:
+        return np.empty_like(v), None
+    if not isinstance(out, np.ndarray) or out.dtype != np.float64 or out.shape != v.shape \
+            or not out.flags.c_contiguous or not out.flags.writeable:
+        raise ValueError("out must be a writeable C-contiguous float64 numpy array shaped like v")
+    return out, None
+
+
+def _ptr(a):
+    return a.data_ptr() if isinstance(a, torch.Tensor) else a.ctypes.data
+
+
+def _host_call(name, v, x, out):
+    v, x = _host_arrays(v, x)
+    out, _ = _host_out(v, out)
+    n = v.numel() if isinstance(v, torch.Tensor) else v.size
+    check(getattr(lib(), name)(_ptr(v), _ptr(x), _ptr(out), n), name)
     return out
 
 
@@ -135,24 +160,11 @@ def log_kv_host(v, x, out=None):
 def log_ivkv_host(v, x, out_i=None, out_k=None):
     """(log I_v(x), log K_v(x)) for HOST float64 arrays in one fused pass: the inputs cross
     PCIe once for both functions."""
-    if isinstance(v, torch.Tensor):
-        if v.is_cuda or x.is_cuda or v.dtype != torch.float64 or x.dtype != torch.float64:
-            raise TypeError("host variants take float64 CPU tensors or numpy arrays")
-        v, x = v.contiguous(), x.contiguous()
-        if v.shape != x.shape:
-            raise ValueError("v and x must have the same shape")
-        out_i = torch.empty_like(v, pin_memory=v.is_pinned()) if out_i is None else out_i
-        out_k = torch.empty_like(v, pin_memory=v.is_pinned()) if out_k is None else out_k
-        ptrs = (v.data_ptr(), x.data_ptr(), out_i.data_ptr(), out_k.data_ptr(), v.numel())
-    else:
-        v = np.ascontiguousarray(v, dtype=np.float64)
-        x = np.ascontiguousarray(x, dtype=np.float64)
-        if v.shape != x.shape:
-            raise ValueError("v and x must have the same shape")
-        out_i = np.empty_like(v) if out_i is None else out_i
-        out_k = np.empty_like(v) if out_k is None else out_k
-        ptrs = (v.ctypes.data, x.ctypes.data, out_i.ctypes.data, out_k.ctypes.data, v.size)
-    check(lib().b200_log_ivkv_f64_host(*ptrs), "b200_log_ivkv_f64_host")
+    v, x = _host_arrays(v, x)
+    out_i, _ = _host_out(v, out_i)
+    out_k, _ = _host_out(v, out_k)
+    n = v.numel() if isinstance(v, torch.Tensor) else v.size
+    check(lib().b200_log_ivkv_f64_host(_ptr(v), _ptr(x), _ptr(out_i), _ptr(out_k), n), "b200_log_ivkv_f64_host")
     return out_i, out_k
 
 
@@ -167,41 +179,53 @@ def _features(X: torch.Tensor):
     return X
 
 
-def vmf_colsum(X: torch.Tensor, out: torch.Tensor | None = None, accumulate: bool = False) -> torch.Tensor:
-    """Column sums of the n x d features in float64 (the data-parallel part of the vMF fit)."""
+def vmf_colsum(X: torch.Tensor, out: torch.Tensor | None = None, accumulate: bool = False,
+               with_count: bool = False) -> torch.Tensor:
+    """Column sums of the n x d features in float64 (the data-parallel part of the vMF fit).
+    with_count: the result has d + 1 entries, the last one (+)= n (one all-reduce carries both)."""
     X = _features(X)
     n, d = X.shape
+    m = d + 1 if with_count else d
     if out is None:
-        out = torch.empty(d, dtype=torch.float64, device=X.device)
+        out = torch.empty(m, dtype=torch.float64, device=X.device)
+    elif (not isinstance(out, torch.Tensor) or not out.is_cuda or out.device != X.device
+          or out.dtype != torch.float64 or out.shape != (m,) or not out.is_contiguous()):
+        raise ValueError(f"out must be a contiguous float64 CUDA tensor of shape ({m},) on X's device")
     fn = lib().b200_vmf_colsum_f64 if X.dtype == torch.float64 else lib().b200_vmf_colsum_f32
     with torch.cuda.device(X.device):
-        check(fn(X.data_ptr(), n, d, X.stride(0), out.data_ptr(), int(accumulate), _stream(X)), "vmf_colsum")
+        check(fn(X.data_ptr(), n, d, X.stride(0), out.data_ptr(), int(accumulate), int(with_count), _stream(X)),
+              "vmf_colsum")
     return out
 
 
-def vmf_fit_from_colsum(colsum: torch.Tensor, n_total: int):
-    """mu (d,) and stats (8,) from the global column sum (§6.3)."""
-    if not colsum.is_cuda or colsum.dtype != torch.float64 or colsum.dim() != 1:
+def vmf_fit_from_colsum(colsum: torch.Tensor, n_total: int | None = None):
+    """mu (d,) and stats (8,) from the global column sum (§6.3).
+    n_total None: colsum is a with_count sum of d + 1 entries whose last entry is the row count."""
+    if not isinstance(colsum, torch.Tensor) or not colsum.is_cuda or colsum.dtype != torch.float64 \
+            or colsum.dim() != 1:
         raise TypeError("colsum must be a 1-D float64 CUDA tensor")
     colsum = colsum.contiguous()
-    d = colsum.numel()
+    d = colsum.numel() - (1 if n_total is None else 0)
+    if n_total is not None and int(n_total) <= 0:
+        raise ValueError("n_total must be positive")
     mu = torch.empty(d, dtype=torch.float64, device=colsum.device)
     stats = torch.empty(8, dtype=torch.float64, device=colsum.device)
     with torch.cuda.device(colsum.device):
-        check(lib().b200_vmf_fit_from_colsum(colsum.data_ptr(), int(n_total), d, mu.data_ptr(),
-                                             stats.data_ptr(), _stream(colsum)), "vmf_fit_from_colsum")
+        check(lib().b200_vmf_fit_from_colsum(colsum.data_ptr(), 0 if n_total is None else int(n_total), d,
+                                             mu.data_ptr(), stats.data_ptr(), _stream(colsum)),
+              "vmf_fit_from_colsum")
     return mu, stats
 
 
 def vmf_fit(X: torch.Tensor, process_group=None):
     """Fit a vMF distribution to the rows of X (unit-norm features).
 
-    With a torch.distributed process group the rows are a shard: the
-    column sums are all-reduced (one NCCL all-reduce of d doubles) and the
-    row count summed, then every rank computes the same fit.
-    Returns (mu, stats) with stats named by VMF_STATS.
+    With a torch.distributed process group the rows are a shard: the column
+    sums and the row count travel in one buffer of d + 1 doubles and ONE
+    all-reduce (NCCL on GPUs) sums them; every rank then computes the same fit
+    on the device.  Returns (mu, stats) with stats named by VMF_STATS.
     """
     from .parallel import allreduce_colsum
     X = _features(X)
-    colsum, n = allreduce_colsum(vmf_colsum(X), X.shape[0], process_group)
-    return vmf_fit_from_colsum(colsum, n)
+    buf = allreduce_colsum(vmf_colsum(X, with_count=True), process_group)
+    return vmf_fit_from_colsum(buf)

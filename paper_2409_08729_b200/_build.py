@@ -14,7 +14,6 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "lib")
 LIB = os.path.join(LIBDIR, "libbessel_b200.so")
 SOURCES = ["bessel_kernels.cu", "vmf_kernels.cu"]
-HEADERS = ["bessel_math.cuh", "tables.h", os.path.join("..", "..", "include", "bessel_b200.h")]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -30,12 +29,20 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found: the CUDA toolkit is required to build libbessel_b200.so")
 
 
+def _deps() -> list[str]:
+    """Every file the library depends on: all of csrc/ (sources and headers), the
+    public header(s) and the table generator."""
+    import glob
+    deps = sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cuh")) +
+                  glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(ROOT, "include", "*.h")))
+    return deps + [os.path.join(PKG, "gen_tables.py"), os.path.abspath(__file__)]
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, s) for s in SOURCES + HEADERS] + [os.path.join(PKG, "gen_tables.py")]
-    return any(os.path.getmtime(d) > t for d in deps if os.path.exists(d))
+    return any(os.path.getmtime(d) > t for d in _deps() if os.path.exists(d))
 
 
 def build(force: bool = False, verbose: bool = False) -> str:

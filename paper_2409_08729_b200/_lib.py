@@ -26,8 +26,8 @@ SIGNATURES = {
     "b200_log_iv_f64_host": [P, P, P, I64],
     "b200_log_kv_f64_host": [P, P, P, I64],
     "b200_log_ivkv_f64_host": [P, P, P, P, I64],
-    "b200_vmf_colsum_f32": [P, I64, I64, I64, P, INT, P],
-    "b200_vmf_colsum_f64": [P, I64, I64, I64, P, INT, P],
+    "b200_vmf_colsum_f32": [P, I64, I64, I64, P, INT, INT, P],
+    "b200_vmf_colsum_f64": [P, I64, I64, I64, P, INT, INT, P],
     "b200_vmf_fit_from_colsum": [P, I64, I64, P, P, P],
     "b200_vmf_fit_f32": [P, I64, I64, P, P, P, P],
     "b200_vmf_fit_f64": [P, I64, I64, P, P, P, P],

@@ -54,11 +54,11 @@ constexpr int BIN_SLOW = 7;           // out-of-range / special inputs (slow_eva
 std::atomic<int64_t> g_launches{0};
 static thread_local char g_err[256] = "";
 
-static int set_err(int code, const char *msg) {
+int set_err(int code, const char *msg) {
     snprintf(g_err, sizeof(g_err), "%s", msg);
     return code;
 }
-static int cuda_err(cudaError_t e, const char *where) {
+int cuda_err(cudaError_t e, const char *where) {
     if (e == cudaSuccess) return B200_OK;
     snprintf(g_err, sizeof(g_err), "%s: %s", where, cudaGetErrorString(e));
     return B200_ERR_CUDA;
@@ -76,11 +76,18 @@ enum : int { FN_I = 0, FN_K = 1, FN_K_PAPER = 2, FN_IK = 3 };   // FN_IK: both, 
 // -- non-finite or out-of-domain inputs and finite arguments outside that
 // range -- goes to bin 7 and through slow_eval (library functions, rescaling).
 // The tests run on the IEEE high words (integer pipe).
-template <int FN>
+// Operating range per precision (R13): f64 [1e-140, 1e140]; f32 [1e-18, 1e18],
+// where v^2 + x^2, 1/x, x/(v + rho) and x^2/4 are still normal floats.
+template <typename T> struct Range;
+template <> struct Range<double> { static constexpr uint32_t lo = B200_HW_LO, hi = B200_HW_HI; };
+template <> struct Range<float> { static constexpr uint32_t lo = B200_HW_LO32, hi = B200_HW_HI32; };
+
+template <typename T, int FN>
 __device__ __forceinline__ int bin_of(double v, double x) {
+    constexpr uint32_t LO = Range<T>::lo, HI = Range<T>::hi;
     const uint32_t hx = hiw(x), hvs = hiw(v), hv = hvs & 0x7FFFFFFFu;
-    if (hx - B200_HW_LO > B200_HW_HI - B200_HW_LO) return BIN_SLOW;    // x outside [1e-140, 1e140] (or <= 0, NaN)
-    if (hv > B200_HW_HI) return BIN_SLOW;                               // |v| > 1e140, inf, NaN
+    if (hx - LO > HI - LO) return BIN_SLOW;                             // x outside the range (or <= 0, NaN)
+    if (hv > HI) return BIN_SLOW;                                       // |v| above the range, inf, NaN
     if ((FN == FN_I || FN == FN_IK) && hvs != hv) return BIN_SLOW;     // v < 0 (or -0.0: handled there)
     return select_eval_hw(fabs(v), x, hv, hx, (FN == FN_I) ? B200_HW_X8 : B200_HW_X2);
 }
@@ -131,7 +138,7 @@ __device__ __forceinline__ T eval_bin(int bin, T v, T x) {
         case E_UC: return log_bessel_u<T, true, KU_C, false>(av, x);
         case E_U13: return log_bessel_u<T, true, 13, false>(av, x);
         case E_FB_A:
-        case E_FB_B: return FN == FN_K_PAPER ? log_kv_integral_paper<T>(av, x) : log_kv_fallback<T>(av, x);
+        case E_FB_B: return FN == FN_K_PAPER ? log_kv_integral_paper<T>(av, x) : log_kv_fallback<T, false>(av, x);
         default: return slow_eval<T, FN>(v, x);
     }
 }
@@ -156,14 +163,17 @@ __device__ __forceinline__ void eval_bin_ik(int bin, T v, T x, T &ri, T &rk) {
         case E_FB_A:   // x <= 2
 #ifndef B200_IK_SERIES_A
             if constexpr (sizeof(T) == 8) {
-                if (x >= T(1e-6) && x <= T(2)) {
+                // v < 1/2 keeps the power series: there |log I| can be << 1 (log I_0(x) ~ x^2/4)
+                // and log I = -log K_mu - log(...) would cancel to an absolute, not relative,
+                // error (R1)
+                if (x >= T(1e-6) && x <= T(2) && v >= T(0.5)) {
                     log_ivkv_trap<T, true>(v, x, ri, rk);   // Temme K values, Wronskian + Miller ratio
                     break;
                 }
             }
 #endif
             ri = log_iv_series<T, false>(v, x);
-            rk = log_kv_fallback<T>(v, x);
+            rk = log_kv_fallback<T, false>(v, x);
             break;
         default:
             ri = slow_eval<T, FN_I>(v, x);
@@ -334,7 +344,7 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
             const int j = tid + i * TPB;
             lb[i] = -1;
             if (j < rem) {
-                lb[i] = bin_of<FN>(double(sv[j]), double(sx[j]));
+                lb[i] = bin_of<T, FN>(double(sv[j]), double(sx[j]));
                 c8 += 1ull << (8 * lb[i]);
             }
         }
@@ -520,7 +530,7 @@ static int host_eval_f64(const double *v_h, const double *x_h, double *out_h, in
         g_pipe.ready = true;
     }
     int64_t chunk = 0;
-    for (int64_t off = 0; off < n; off += HostPipe::CH, ++chunk) {
+    for (int64_t off = 0; off < n && rc == B200_OK; off += HostPipe::CH, ++chunk) {
         const int slot = int(chunk % HostPipe::NSLOT);
         const int64_t m = (n - off < HostPipe::CH) ? n - off : HostPipe::CH;
         double *dv = static_cast<double *>(g_pipe.buf[slot]);
@@ -529,19 +539,23 @@ static int host_eval_f64(const double *v_h, const double *x_h, double *out_h, in
         double *dout2 = dout + HostPipe::CH;
         cudaStream_t s = g_pipe.st[slot];
         if ((rc = cuda_err(cudaMemcpyAsync(dv, v_h + off, m * sizeof(double), cudaMemcpyHostToDevice, s), "H2D")))
-            return rc;
+            break;
         if ((rc = cuda_err(cudaMemcpyAsync(dx, x_h + off, m * sizeof(double), cudaMemcpyHostToDevice, s), "H2D")))
-            return rc;
-        if ((rc = launch_eval<double, FN>(dv, dx, dout, m, s, dout2))) return rc;
+            break;
+        if ((rc = launch_eval<double, FN>(dv, dx, dout, m, s, dout2))) break;
         if ((rc = cuda_err(cudaMemcpyAsync(out_h + off, dout, m * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H")))
-            return rc;
+            break;
         if (FN == FN_IK &&
             (rc = cuda_err(cudaMemcpyAsync(out2_h + off, dout2, m * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H")))
-            return rc;
+            break;
     }
-    for (int i = 0; i < HostPipe::NSLOT; ++i)
-        if ((rc = cuda_err(cudaStreamSynchronize(g_pipe.st[i]), "sync"))) return rc;
-    return B200_OK;
+    // drain every slot, on success and on error alike: no copy into the caller's
+    // buffers may still be running when this returns
+    for (int i = 0; i < HostPipe::NSLOT; ++i) {
+        const int r = cuda_err(cudaStreamSynchronize(g_pipe.st[i]), "sync");
+        if (rc == B200_OK) rc = r;
+    }
+    return rc;
 }
 
 }  // namespace b200

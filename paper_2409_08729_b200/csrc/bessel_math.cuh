@@ -239,8 +239,15 @@ __device__ __forceinline__ T v_times_eta(T v, T x, T vs, T xs, T rhos, T rho) {
         for (int k = EtaC<T>::nt - 2; k >= 0; --k) p = fma(p, d, EtaC<T>::c(k));
         return v * (p * d);
     }
+    if constexpr (SAFE) {
+        // log(x/(v + rho)): the quotient underflows when x << v (subnormal x, huge v);
+        // then take the difference of the logs of the (scaled, normal) operands
+        const T den = vs + rhos;
+        const T lq = xs >= T(1e-30) * den ? fm_log_wide(xs * fm_rcp(den)) : log(xs) - log(den);
+        return fma(v, lq, rho);
+    }
     const T q = xs * fm_rcp(vs + rhos);
-    return fma(v, SAFE ? fm_log_wide(q) : fm_log(q), rho);
+    return fma(v, fm_log(q), rho);
 }
 
 // Number of U_K terms.  The paper's Table 1 fits regions for U4/U6/U9/U13 and
@@ -256,15 +263,17 @@ __device__ __forceinline__ T v_times_eta(T v, T x, T vs, T xs, T rhos, T rho) {
 
 template <typename T, bool IS_K, int KU, bool SAFE>
 __device__ __forceinline__ T log_bessel_u(T v, T x) {
-    // rescale by a power of two where v^2 + x^2 could overflow (wide-range guard)
+    // rescale by s = 2^-e, e = the binary exponent of max(v, x), where v^2 + x^2 could
+    // overflow (wide-range guard): then max(vs, xs) is in [1, 2)
     const bool big = SAFE && fmax(v, x) >= Big<T>::v;
-    const T s = big ? T(1.0 / 1267650600228229401496703205376.0) : T(1);     // 2^-100
-    const T ls = big ? T(-69.31471805599453) : T(0);                         // log s
+    const int e = big ? ilogb(fmax(v, x)) : 0;
+    const T s = big ? T(scalbn(1.0, -e)) : T(1);
+    const T ls = big ? T(-double(e) * 0.6931471805599453) : T(0);          // log s
     const T vs = v * s, xs = x * s;
     const T rho2 = fma(vs, vs, xs * xs);
     const T y = fm_rsqrt(rho2);                  // 1 / (s rho)
     const T rhos = rho2 * y;
-    const T rho = big ? rhos * T(1267650600228229401496703205376.0) : rhos;
+    const T rho = big ? T(scalbn(double(rhos), e)) : rhos;
     const T t = vs * y;
     const T t2 = t * t;
     const T w = (IS_K ? -y : y) * s;             // +-t/v
@@ -362,7 +371,9 @@ __device__ __forceinline__ T log_iv_series(T v, T x) {
     if (x == T(0)) return v == T(0) ? T(0) : T(-CUDART_INF);
     if constexpr (sizeof(T) == 8) {
         const T q = T(0.25) * x * x;
-        T N = T(1), P = T(1), Q = T(1), vk = v, kd = T(0);
+        // M_k = N_k - P_k = P_k sum_{1<=j<=k} b_j (carried instead of N: the sum minus its
+        // leading 1 keeps full relative accuracy when the sum is ~1, e.g. log I_0(x) ~ x^2/4)
+        T M = T(0), P = T(1), Q = T(1), vk = v, kd = T(0);
         for (int k = 1; k < 400; k += 4) {      // four terms per trip, one stop test
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -370,16 +381,27 @@ __device__ __forceinline__ T log_iv_series(T v, T x) {
                 kd += T(1);
                 const T d = kd * vk;
                 Q *= q;
-                N = fma(N, d, Q);
+                M = fma(M, d, Q);
                 P *= d;
             }
-            if (Q <= N * Tr<T>::eps) break;
+            if (Q <= (M + P) * Tr<T>::eps) break;
         }
         // a_0 = 1/Gamma(v+1) = rg(mu) / prod_{j=1..n} (mu + j), v = n + mu, |mu| <= 1/2,
-        // rg(z) = 1/Gamma(1+z) by its Taylor series (tables.h) -- no lgamma call
+        // rg(z) = 1/Gamma(1+z) by its Taylor series (tables.h) -- no lgamma call;
+        // rg(mu) = 1 + gm1 with gm1 = mu (c_1 + mu (c_2 + ...)) (c_0 = 1)
         const T fl = floor(v + T(0.5));
         const T mu = v - fl;
         const int nl = int(fl);
+        T g = T(c_rg_d[B200_RGAMMA_NT - 1]);
+#pragma unroll
+        for (int j = B200_RGAMMA_NT - 2; j >= 1; --j) g = fma(g, mu, T(c_rg_d[j]));
+        const T gm1 = g * mu;
+        const T lx = SAFE ? fm_log_wide(x) - T(0.6931471805599453) : fm_log(T(0.5) * x);   // log(x/2)
+        if (nl == 0) {
+            // v < 1/2: log I = v log(x/2) + log1p(gm1) + log1p(M/P) -- every term with
+            // relative accuracy (|log I| < 1 here for small v and x: DESIGN.md R1)
+            return fma(v, lx, fm_log1p(gm1) + fm_log1p(fm_div(M, P)));
+        }
         T pr = T(1), m = mu;
         for (int j = 1; j < nl; j += 2) {      // factor pairs (mu+j)(mu+j+1)
             const T a = m + T(1);
@@ -387,11 +409,7 @@ __device__ __forceinline__ T log_iv_series(T v, T x) {
             pr *= a * m;
         }
         if (nl & 1) pr *= m + T(1);
-        T g = T(c_rg_d[B200_RGAMMA_NT - 1]);
-#pragma unroll
-        for (int j = B200_RGAMMA_NT - 2; j >= 0; --j) g = fma(g, mu, T(c_rg_d[j]));
-        const T lx = SAFE ? fm_log_wide(T(0.5) * x) : fm_log(T(0.5) * x);
-        return fma(v, lx, fm_log(fm_div(N * g, P * pr)));
+        return fma(v, lx, fm_log(fm_div((M + P) * (T(1) + gm1), P * pr)));
     }
     const T q = T(0.25) * x * x;
     T b = T(1), S = T(1);
@@ -405,7 +423,8 @@ __device__ __forceinline__ T log_iv_series(T v, T x) {
         S += b0 + b;
         if (r1 < T(1) && b <= S * Tr<T>::eps) break;
     }
-    return v * log(T(0.5) * x) - d_lgamma(v + T(1)) + log(S);
+    const T lx = SAFE ? log(x) - T(0.6931471805599453) : log(T(0.5) * x);   // log(x/2); 0.5 x underflows for tiny x
+    return (v == T(0) ? T(0) : v * lx) - d_lgamma(v + T(1)) + log(S);
 }
 
 // ---------------------------------------------------------------- K fallback
@@ -459,13 +478,23 @@ __device__ __forceinline__ void sinhc_cosh(T e, T E, T &shc, T &ch) {
     }
 }
 
-// returns log K_mu(x) and rho = K_{mu+1}(x) / K_mu(x), for 0 < x <= 2 (Temme's series).
-// Elementary functions from fastmath.cuh (x >= 1e-140 on the fast path, so
-// ln(2/x) <= 323, |mu ln(2/x)| <= 162, every reciprocal argument normal).
-template <typename T>
-__device__ __forceinline__ T temme_kmu(T mu, T x, T &rho) {
+// Temme's series for K_mu, K_{mu+1}, |mu| <= 1/2, 0 < x <= 2: N. M. Temme, "On the
+// numerical evaluation of the modified Bessel function of the third kind",
+// J. Comput. Phys. 19 (1975) 324-337; the step order follows the published
+// formulation (f_k, p_k, q_k recurrences; the same lineage as Numerical Recipes'
+// bessik and libstdc++'s tr1 __bessel_ik).  Re-worked for the GPU: one shared
+// reciprocal of i^2 - mu^2 per term, multiplicative p/q updates, two terms per
+// stop test, 1/Gamma(1 +- mu) and pi mu / sin(pi mu) from Taylor tables.
+// Returns log K_mu(x) and the sums S = K_mu(x), S1 with K_{mu+1}(x) = (2/x) S1
+// (callers form rho = K_{mu+1}/K_mu = 2 S1 / (x S), or the scaled ratio S1 / S).
+// SAFE = false: elementary functions from fastmath.cuh (x >= 1e-140 on the fast
+// path, so ln(2/x) <= 323, |mu ln(2/x)| <= 162, every reciprocal argument normal).
+// SAFE = true (the slow bin): any x > 0 including subnormals -- ln(2/x) = ln 2 -
+// log x by the library log (0.5 x would underflow), |mu ln(2/x)| <= 372.5.
+template <typename T, bool SAFE = false>
+__device__ __forceinline__ T temme_kmu(T mu, T x, T &sum, T &sum1) {
     const T eps = Tr<T>::eps;
-    const T d = -fm_log(T(0.5) * x);                          // ln(2/x)
+    const T d = SAFE ? T(0.6931471805599453) - log(x) : -fm_log(T(0.5) * x);   // ln(2/x)
     const T e = mu * d;
     // pi mu / sin(pi mu) = 1 / sum_k SINPI[k] mu^(2k)  (|mu| <= 1/2, tables.h)
     const T m2 = mu * mu;
@@ -479,12 +508,12 @@ __device__ __forceinline__ T temme_kmu(T mu, T x, T &rho) {
     T gam1, gam2, gampl, gammi;
     temme_gammas<T>(mu, gam1, gam2, gampl, gammi);
     T ff = fact * (gam1 * che + gam2 * fact2 * d);
-    T sum = ff;
+    sum = ff;
     T p = T(0.5) * ee * fm_rcp(gampl);                        // 1/2 (2/x)^mu Gamma(1+mu)
     T q = T(0.5) * fm_rcp(ee * gammi);                        // 1/2 (x/2)^mu Gamma(1-mu)
     T c = T(1);
     const T dd = T(0.25) * x * x;
-    T sum1 = p;
+    sum1 = p;
     T fi = T(0);
     for (int i = 1; i < 100; i += 2) {          // two terms per stop test
         T del;
@@ -503,8 +532,7 @@ __device__ __forceinline__ T temme_kmu(T mu, T x, T &rho) {
         }
         if (fabs(del) < fabs(sum) * eps) break;
     }
-    rho = T(2) * sum1 * fm_rcp(x * sum);
-    return fm_log(sum);
+    return SAFE ? log(sum) : fm_log(sum);
 }
 
 // K_mu(x) and K_{mu+1}(x), |mu| <= 1/2, on the band 2 < x <= 30 of the
@@ -562,16 +590,16 @@ __device__ __forceinline__ T trap_kmu(T mu, T x, T &rho) {
     return -x + fm_log(T(0.5) * h * A);
 }
 
-template <typename T>
+template <typename T, bool SAFE>
 __device__ __forceinline__ T log_kv_fallback(T v, T x) {
     const int nl = int(floor(v + T(0.5)));
     const T mu = v - T(nl);
-    T rho;
-    const T tox = T(2) * fm_rcp(x);
     // forward recurrence K_{nu+1} = K_{nu-1} + (2 nu / x) K_nu (stable for K)
     // on the ratios K_{mu+i} / K_mu, from i = 0, 1 up to i = nl
     if (x > T(2)) {
+        T rho;
         const T lk = trap_kmu<T>(mu, x, rho);
+        const T tox = T(2) * fm_rcp(x);
         // x > 2, v <= 12.7: K_v / K_mu < 1e12, no rescaling needed
         T km = T(1), kp = rho, nu = mu;
         for (int i = 1; i < nl; ++i) {
@@ -582,39 +610,41 @@ __device__ __forceinline__ T log_kv_fallback(T v, T x) {
         }
         return nl == 0 ? lk : lk + fm_log(kp);
     }
-    const T lk = temme_kmu<T>(mu, x, rho);
+    T S, S1;
+    const T lk = temme_kmu<T, SAFE>(mu, x, S, S1);
     if (nl == 0) return lk;
-    // small x: each step multiplies by up to 2 nu / x (<= 3e141), so the ratio
-    // (in double for both precisions) is renormalised by an exact power of two
-    // whenever it passes 2^400
-    double km = 1.0, kp = double(rho), nu = double(mu);
-    const double tx = double(tox);
-    int e2 = 0;
     if (x >= T(1e-6)) {
-        // (2 * 13 / 1e-6)^13 < 2^400: no renormalisation needed
+        // (2 * 13 / 1e-6)^13 < 1e97: the unscaled ratio stays in the double range
+        // (double for both precisions)
+        const double tx = double(T(2) * fm_rcp(x));
+        double km = 1.0, kp = double(T(2) * S1 * fm_rcp(x * S)), nu = double(mu);
         for (int i = 1; i < nl; ++i) {
             nu += 1.0;
             const double kn = fma(nu * tx, kp, km);
             km = kp;
             kp = kn;
         }
-    } else {
-        for (int i = 1; i < nl; ++i) {
-            nu += 1.0;
-            const double kn = fma(nu * tx, kp, km);
-            km = kp;
-            kp = kn;
-            if (kp > 2.5822498780869086e120) {                // 2^400
-                const int k = ilogb(kp);
-                const double sc = scalbn(1.0, -k);
-                km *= sc;
-                kp *= sc;
-                e2 += k;
-            }
-        }
+        return lk + T(fm_log(kp));
     }
-    // kp = K_v / K_mu * 2^-e2
-    return lk + T(fm_log(kp) + double(e2) * 0.6931471805599453);
+    // x < 1e-6 (any x > 0, subnormals included): scaled ratios.  With s = x/2 and
+    // a = 2 max(-mu, 0), k_i = (K_{mu+i}/K_mu) s^(i-a) (i >= 1) is O(1) for every i
+    // (K_{mu+i} ~ Gamma(mu+i) (2/x)^(mu+i) / 2 and K_mu ~ Gamma(|mu|) (2/x)^|mu| / 2), so
+    // nothing overflows or underflows even at x = 5e-324:
+    //   k_1 = (S1/S) s^-a,  k_2 = s^(2-a) + (mu+1) k_1,  k_{i+1} = s^2 k_{i-1} + (mu+i) k_i,
+    //   log K_v = log K_mu + log k_nl - (nl - a) log s.
+    const double ls = (SAFE ? fm_log_wide(double(x)) : fm_log(double(x))) - 0.6931471805599453;   // log(x/2)
+    const double a = mu < T(0) ? -2.0 * double(mu) : 0.0;
+    const double k1 = mu < T(0) ? fm_exp(fm_log(double(S1)) - fm_log(double(S)) - a * ls) : double(S1) / double(S);
+    if (nl == 1) return lk + T(fm_log(k1) - (1.0 - a) * ls);
+    const double s2 = 0.25 * double(x) * double(x);   // underflows harmlessly for tiny x
+    double km = k1, kp = fm_exp((2.0 - a) * ls) + double(mu + T(1)) * k1, nu = double(mu) + 1.0;
+    for (int i = 2; i < nl; ++i) {
+        nu += 1.0;
+        const double kn = fma(s2, km, nu * kp);
+        km = kp;
+        kp = kn;
+    }
+    return lk + T(fm_log(kp) - (double(nl) - a) * ls);
 }
 
 // Fused fallback for 2 < x <= 30, v <= 12.7 (FN_IK): log K_v as in
@@ -638,7 +668,14 @@ __device__ __forceinline__ void log_ivkv_trap(T v, T x, T &ri, T &rk) {
     const T mu = v - T(nl);
     const T tox = T(2) * fm_rcp(x);
     T rho;
-    const T lk = TEMME ? temme_kmu<T>(mu, x, rho) : trap_kmu<T>(mu, x, rho);
+    T lk;
+    if constexpr (TEMME) {
+        T S, S1;
+        lk = temme_kmu<T>(mu, x, S, S1);
+        rho = T(2) * S1 * fm_rcp(x * S);
+    } else {
+        lk = trap_kmu<T>(mu, x, rho);
+    }
     // kp = K_v / K_mu, kn = K_{v+1} / K_mu (one recurrence step past v)
     T km = T(1), kp = rho, nu = mu;
     for (int i = 1; i <= nl; ++i) {
@@ -758,7 +795,7 @@ __device__ __forceinline__ T log_kv_eval(int e, T v, T x) {
         case E_UB: return log_bessel_u<T, true, KU_B, SAFE>(v, x);
         case E_UC: return log_bessel_u<T, true, KU_C, SAFE>(v, x);
         case E_U13: return log_bessel_u<T, true, 13, SAFE>(v, x);
-        default: return PAPER ? log_kv_integral_paper<T>(v, x) : log_kv_fallback<T>(v, x);
+        default: return PAPER ? log_kv_integral_paper<T>(v, x) : log_kv_fallback<T, SAFE>(v, x);
     }
 }
 

@@ -147,6 +147,14 @@ __device__ __forceinline__ double fm_rsqrt(double a) {
     return fma(0.5 * y, e, y);                // Newton step
 }
 
+// log(1 + d) for d > -1 with relative accuracy when |d| is small: u = 1 + d rounds,
+// the first-order correction restores the lost low part of d (u - 1 is exact).
+__device__ __forceinline__ double fm_log1p(double d) {
+    const double u = 1.0 + d;
+    if (u == 1.0) return d;
+    return fm_log(u) - ((u - 1.0) - d) * fm_rcp(u);
+}
+
 // log(a) for any finite a > 0 (subnormals through the library function).
 __device__ __forceinline__ double fm_log_wide(double a) { return a >= 1e-300 ? fm_log(a) : log(a); }
 

@@ -19,6 +19,8 @@
 namespace b200 {
 
 extern std::atomic<int64_t> g_launches;   // defined in bessel_kernels.cu
+int set_err(int code, const char *msg);    // bessel_kernels.cu: per-thread last-error string
+int cuda_err(cudaError_t e, const char *where);
 
 constexpr int CS_TPB = 256;
 
@@ -143,7 +145,7 @@ __global__ void __launch_bounds__(FIT_TPB) vmf_fit_kernel(const double *__restri
     __shared__ double s_red[FIT_TPB / 32];
     __shared__ double s_rbar;
     __shared__ double s_l[2];
-    const double inv_n = 1.0 / double(n_total);
+    const double inv_n = 1.0 / (n_total > 0 ? double(n_total) : colsum[d]);
     double loc = 0.0;
     for (int64_t j = threadIdx.x; j < d; j += blockDim.x) {
         const double m = colsum[j] * inv_n;
@@ -215,68 +217,111 @@ __global__ void __launch_bounds__(FIT_TPB) vmf_fit_kernel(const double *__restri
 }
 
 // ---------------------------------------------------------------- scratch
-struct Scratch {
-    std::mutex mu;
-    int dev = -1;
-    void *ptr = nullptr;
-    size_t bytes = 0;
+// The per-slab partials live in a scratch buffer owned by the library, one per
+// (device, stream): calls on one stream are ordered by the stream, and the
+// mutex is held while a call enqueues both of its kernels, so two host threads
+// sharing a stream cannot interleave partial / reduce pairs.  Calls on
+// different streams use different buffers (no race).  A buffer that must grow
+// is freed only after its stream has drained; buffers live for the process.
+struct ScratchEnt {
+    int dev;
+    cudaStream_t stream;
+    void *ptr;
+    size_t bytes;
 };
-static Scratch g_scratch;
+constexpr int SCRATCH_MAX = 256;
+static std::mutex g_scratch_mu;
+static ScratchEnt g_scratch[SCRATCH_MAX];
+static int g_nscratch = 0;
 
-static int scratch_get(size_t bytes, double **out) {
-    std::lock_guard<std::mutex> lk(g_scratch.mu);
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (g_scratch.dev != dev || g_scratch.bytes < bytes) {
-        if (g_scratch.ptr && g_scratch.dev == dev) cudaFree(g_scratch.ptr);
-        g_scratch.ptr = nullptr;
-        g_scratch.bytes = 0;
-        cudaError_t e = cudaMalloc(&g_scratch.ptr, bytes);
-        if (e != cudaSuccess) return B200_ERR_CUDA;
-        g_scratch.bytes = bytes;
-        g_scratch.dev = dev;
+// Called with g_scratch_mu held.
+static int scratch_get(int dev, cudaStream_t s, size_t bytes, double **out) {
+    ScratchEnt *e = nullptr;
+    for (int i = 0; i < g_nscratch; ++i)
+        if (g_scratch[i].dev == dev && g_scratch[i].stream == s) { e = &g_scratch[i]; break; }
+    if (!e) {
+        if (g_nscratch == SCRATCH_MAX) {
+            // evict the oldest entry: wait for its stream's work, then free it
+            ScratchEnt &o = g_scratch[0];
+            int cur = 0;
+            cudaGetDevice(&cur);
+            cudaSetDevice(o.dev);
+            cudaStreamSynchronize(o.stream);
+            cudaFree(o.ptr);
+            cudaSetDevice(cur);
+            for (int i = 1; i < g_nscratch; ++i) g_scratch[i - 1] = g_scratch[i];
+            --g_nscratch;
+        }
+        e = &g_scratch[g_nscratch++];
+        *e = ScratchEnt{dev, s, nullptr, 0};
     }
-    *out = static_cast<double *>(g_scratch.ptr);
+    if (e->bytes < bytes) {
+        if (e->ptr) {
+            cudaError_t err = cudaStreamSynchronize(s);          // earlier calls may still read it
+            if (err != cudaSuccess) return cuda_err(err, "vmf scratch: cudaStreamSynchronize");
+            cudaFree(e->ptr);
+            e->ptr = nullptr;
+            e->bytes = 0;
+        }
+        cudaError_t err = cudaMalloc(&e->ptr, bytes);
+        if (err != cudaSuccess) return cuda_err(err, "vmf scratch: cudaMalloc");
+        e->bytes = bytes;
+    }
+    *out = static_cast<double *>(e->ptr);
     return B200_OK;
 }
 
-static int sms_count() {
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
+static int sms_count(int dev) {
+    constexpr int MAXDEV = 64;
+    static std::atomic<int> sms[MAXDEV];
+    if (dev < 0 || dev >= MAXDEV) return 148;
+    int v = sms[dev].load(std::memory_order_relaxed);
+    if (!v) {
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+        sms[dev].store(v, std::memory_order_relaxed);
     }
-    return sms;
+    return v;
+}
+
+// colsum[d] (+)= n as a double when with_count: the row count travels in the same
+// buffer, so a sharded fit needs exactly one all-reduce of d + 1 doubles.
+__global__ void count_slot_kernel(double *slot, double n, int accumulate) {
+    *slot = accumulate ? *slot + n : n;
 }
 
 template <typename T>
 static int colsum_impl(const T *X, int64_t n, int64_t d, int64_t ld, double *colsum, int accumulate,
-                       cudaStream_t s) {
-    if (n < 0 || d < 0 || ld < d) return B200_ERR_INVALID_ARGUMENT;
+                       int with_count, cudaStream_t s) {
+    if (n < 0 || d < 0 || ld < d) return set_err(B200_ERR_INVALID_ARGUMENT, "vmf_colsum: n < 0, d < 0 or ld < d");
+    if (d == 0 && !with_count) return B200_OK;
+    if (!X && n > 0) return set_err(B200_ERR_INVALID_ARGUMENT, "vmf_colsum: null X");
+    if (!colsum) return set_err(B200_ERR_INVALID_ARGUMENT, "vmf_colsum: null colsum");
+    if (with_count) {
+        count_slot_kernel<<<1, 1, 0, s>>>(colsum + d, double(n), accumulate);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_err(e, "count_slot_kernel launch");
+    }
     if (d == 0) return B200_OK;
-    if (!X && n > 0) return B200_ERR_INVALID_ARGUMENT;
-    if (!colsum) return B200_ERR_INVALID_ARGUMENT;
     if (n == 0) {
-        if (!accumulate) {
-            cudaError_t e = cudaMemsetAsync(colsum, 0, size_t(d) * sizeof(double), s);
-            return e == cudaSuccess ? B200_OK : B200_ERR_CUDA;
-        }
+        if (!accumulate) return cuda_err(cudaMemsetAsync(colsum, 0, size_t(d) * sizeof(double), s), "cudaMemsetAsync");
         return B200_OK;
     }
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return set_err(B200_ERR_NO_DEVICE, "no current CUDA device");
     constexpr int VN = VecOf<T>::N;
     const bool vec = ((reinterpret_cast<uintptr_t>(X) % 16) == 0) && ((ld * sizeof(T)) % 16 == 0);
     const int CW = CS_TPB * (vec ? VN : 1);
     const int64_t ncol = (d + CW - 1) / CW;
     // ~8 CTAs per SM in total; each CTA streams a slab of rows
-    int64_t nslab = (8 * int64_t(sms_count()) + ncol - 1) / ncol;
+    int64_t nslab = (8 * int64_t(sms_count(dev)) + ncol - 1) / ncol;
     if (nslab > n) nslab = n;
     if (nslab < 1) nslab = 1;
     const int64_t rows_per = (n + nslab - 1) / nslab;
     nslab = (n + rows_per - 1) / rows_per;
+    std::lock_guard<std::mutex> lk(g_scratch_mu);   // held over both launches (see scratch_get)
     double *part = nullptr;
-    int rc = scratch_get(size_t(nslab) * size_t(d) * sizeof(double), &part);
+    int rc = scratch_get(dev, s, size_t(nslab) * size_t(d) * sizeof(double), &part);
     if (rc) return rc;
     dim3 grid((unsigned)ncol, (unsigned)nslab);
     if (vec)
@@ -286,15 +331,17 @@ static int colsum_impl(const T *X, int64_t n, int64_t d, int64_t ld, double *col
     const int64_t rb = (d + 31) / 32;
     colsum_reduce_kernel<<<unsigned(rb < 4096 ? rb : 4096), 32 * CR_WARPS, 0, s>>>(part, nslab, d, colsum, accumulate);
     g_launches.fetch_add(2, std::memory_order_relaxed);
-    return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ERR_CUDA;
+    return cuda_err(cudaGetLastError(), "vmf colsum launch");
 }
 
 static int fit_from_colsum_impl(const double *colsum, int64_t n_total, int64_t d, double *mu, double *stats,
                                 cudaStream_t s) {
-    if (n_total <= 0 || d < 2 || !colsum || !mu || !stats) return B200_ERR_INVALID_ARGUMENT;
+    if (d < 2 || !colsum || !mu || !stats) return set_err(B200_ERR_INVALID_ARGUMENT, "vmf_fit: d < 2 or null pointer");
+    if (n_total < 0) return set_err(B200_ERR_INVALID_ARGUMENT, "vmf_fit: n_total < 0");
+    // n_total == 0: the row count is read from colsum[d] (b200_vmf_colsum_* with with_count)
     vmf_fit_kernel<<<1, FIT_TPB, 0, s>>>(colsum, n_total, d, mu, stats);
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    return cudaGetLastError() == cudaSuccess ? B200_OK : B200_ERR_CUDA;
+    return cuda_err(cudaGetLastError(), "vmf_fit_kernel launch");
 }
 
 }  // namespace b200
@@ -304,24 +351,26 @@ using namespace b200;
 extern "C" {
 
 int b200_vmf_colsum_f32(const float *X, int64_t n, int64_t d, int64_t ld, double *colsum, int accumulate,
-                        void *stream) {
-    return colsum_impl<float>(X, n, d, ld, colsum, accumulate, static_cast<cudaStream_t>(stream));
+                        int with_count, void *stream) {
+    return colsum_impl<float>(X, n, d, ld, colsum, accumulate, with_count, static_cast<cudaStream_t>(stream));
 }
 int b200_vmf_colsum_f64(const double *X, int64_t n, int64_t d, int64_t ld, double *colsum, int accumulate,
-                        void *stream) {
-    return colsum_impl<double>(X, n, d, ld, colsum, accumulate, static_cast<cudaStream_t>(stream));
+                        int with_count, void *stream) {
+    return colsum_impl<double>(X, n, d, ld, colsum, accumulate, with_count, static_cast<cudaStream_t>(stream));
 }
 int b200_vmf_fit_from_colsum(const double *colsum, int64_t n_total, int64_t d, double *mu, double *stats,
                              void *stream) {
     return fit_from_colsum_impl(colsum, n_total, d, mu, stats, static_cast<cudaStream_t>(stream));
 }
 int b200_vmf_fit_f32(const float *X, int64_t n, int64_t d, double *ws, double *mu, double *stats, void *stream) {
-    int rc = colsum_impl<float>(X, n, d, d, ws, 0, static_cast<cudaStream_t>(stream));
+    if (n <= 0) return set_err(B200_ERR_INVALID_ARGUMENT, "vmf_fit: n <= 0");
+    int rc = colsum_impl<float>(X, n, d, d, ws, 0, 0, static_cast<cudaStream_t>(stream));
     if (rc) return rc;
     return fit_from_colsum_impl(ws, n, d, mu, stats, static_cast<cudaStream_t>(stream));
 }
 int b200_vmf_fit_f64(const double *X, int64_t n, int64_t d, double *ws, double *mu, double *stats, void *stream) {
-    int rc = colsum_impl<double>(X, n, d, d, ws, 0, static_cast<cudaStream_t>(stream));
+    if (n <= 0) return set_err(B200_ERR_INVALID_ARGUMENT, "vmf_fit: n <= 0");
+    int rc = colsum_impl<double>(X, n, d, d, ws, 0, 0, static_cast<cudaStream_t>(stream));
     if (rc) return rc;
     return fit_from_colsum_impl(ws, n, d, mu, stats, static_cast<cudaStream_t>(stream));
 }

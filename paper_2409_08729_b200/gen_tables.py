@@ -131,6 +131,9 @@ THRESHOLDS = {
     "X30": 30.0, "V15": 15.3919, "X59": 59.6925, "X19": 19.6931, "V07": 0.7, "V12": 12.6964,
     "X8": 8.0, "X2": 2.0, "X1E30": 1e30,
     "LO": 1e-140, "HI": 1e140,
+    # f32 operating range (R13): every fast-path intermediate of the
+    # float kernels (v^2 + x^2, 1/x, x/(v + rho), x^2/4) stays a normal float
+    "LO32": 1e-18, "HI32": 1e18,
 }
 
 

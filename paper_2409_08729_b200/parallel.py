@@ -4,8 +4,8 @@
   (BASELINE north_star: "Batches are sharded contiguously across the GPUs ...
   with no communication").
 * The vMF fit shards its N rows; the only exchange is one all-reduce of the
-  d-vector of column sums (plus the row count), over NCCL on GPUs (gloo in the
-  CPU tests).  Every rank then runs the same scalar fit.
+  d column sums with the row count appended (d + 1 doubles), over NCCL on GPUs
+  (gloo in the CPU tests).  Every rank then runs the same scalar fit.
 """
 from __future__ import annotations
 
@@ -21,12 +21,11 @@ def shard_range(n: int, world: int, rank: int) -> tuple[int, int]:
     return lo, lo + base + (1 if rank < extra else 0)
 
 
-def allreduce_colsum(colsum: torch.Tensor, n_local: int, group=None) -> tuple[torch.Tensor, int]:
-    """Sum the per-rank column sums in place and the row counts; returns (colsum, n_total)."""
+def allreduce_colsum(buf: torch.Tensor, group=None) -> torch.Tensor:
+    """Sum the per-rank [column sums..., row count] buffers (d + 1 doubles, the
+    with_count layout of b200_vmf_colsum_*) in place with ONE all-reduce."""
     import torch.distributed as dist
     if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
-        return colsum, int(n_local)
-    dist.all_reduce(colsum, group=group)
-    cnt = torch.tensor([float(n_local)], dtype=torch.float64, device=colsum.device)
-    dist.all_reduce(cnt, group=group)
-    return colsum, int(round(cnt.item()))
+        return buf
+    dist.all_reduce(buf, group=group)
+    return buf

@@ -37,6 +37,28 @@ def bench_grid(n_per_v: int = 20_000_000, seed: int = 0, device="cuda", dtype=to
     return v, x
 
 
+def bench_grid_slice(n_per_v: int, lo: int, hi: int, seed: int = 0, device="cuda", dtype=torch.float64,
+                     orders=BENCH_ORDERS):
+    """Elements [lo, hi) of ONE global v-major bench grid (the strong-scaling leg:
+    every world size evaluates the same pairs).  The x of order j come from a
+    generator seeded by (seed, j), so any contiguous slice is reproducible alone."""
+    nv = len(orders)
+    if not (0 <= lo <= hi <= nv * n_per_v):
+        raise ValueError("slice out of range")
+    vs, xs = [], []
+    for j in range(lo // n_per_v, (hi + n_per_v - 1) // n_per_v if hi > lo else lo // n_per_v):
+        a, b = max(lo, j * n_per_v), min(hi, (j + 1) * n_per_v)
+        g = torch.Generator(device=device)
+        g.manual_seed(seed * 1_000_003 + j + 1)
+        x = torch.empty(n_per_v, dtype=dtype, device=device).uniform_(1.0, 100.0, generator=g)
+        xs.append(x[a - j * n_per_v:b - j * n_per_v].clone())
+        vs.append(torch.full((b - a,), orders[j], dtype=dtype, device=device))
+        del x
+    if not vs:
+        return torch.empty(0, dtype=dtype, device=device), torch.empty(0, dtype=dtype, device=device)
+    return torch.cat(vs), torch.cat(xs)
+
+
 def bench_grid_numpy(n_per_v: int, seed: int = 0, orders=BENCH_ORDERS):
     rng = np.random.default_rng(seed)
     v = np.repeat(np.asarray(orders, dtype=np.float64), n_per_v)
@@ -82,19 +104,34 @@ def stability_grid(nv: int = 16384, nx: int = 16384, device="cuda", dtype=torch.
     return v, x
 
 
-def vmf_features(n: int, d: int, rbar: float = 0.15, seed: int = 0, device="cuda", dtype=torch.float32):
-    """Rows x_i = normalize(c mu + z_i), z_i ~ N(0, I/d), c = rbar / sqrt(1 - rbar^2)."""
+def vmf_features(n: int, d: int, rbar: float = 0.15, seed: int = 0, device="cuda", dtype=torch.float32,
+                 rows=None):
+    """Rows x_i = normalize(c mu + z_i), z_i ~ N(0, I/d), c = rbar / sqrt(1 - rbar^2).
+
+    The matrix is defined row-chunk by row-chunk: mu comes from `seed` alone and
+    chunk k (a fixed number of rows for a given d) from its own generator
+    seeded by (seed, k), so `rows=(lo, hi)` returns exactly rows lo..hi-1 of the
+    full n x d matrix -- a rank's shard is a slice of the one matrix the N = 1
+    run fits, whatever the world size.
+    """
+    lo, hi = (0, n) if rows is None else rows
+    if not (0 <= lo <= hi <= n):
+        raise ValueError("rows out of range")
     g = torch.Generator(device=device)
     g.manual_seed(seed)
     mu = torch.randn(d, generator=g, device=device, dtype=torch.float64)
     mu /= mu.norm()
     c = rbar / math.sqrt(1.0 - rbar * rbar)
-    X = torch.empty(n, d, device=device, dtype=dtype)
-    chunk = max(1, (1 << 28) // (d * 8))
-    for i in range(0, n, chunk):
-        m = min(chunk, n - i)
-        z = torch.randn(m, d, generator=g, device=device, dtype=torch.float64) / math.sqrt(d)
+    X = torch.empty(hi - lo, d, device=device, dtype=dtype)
+    chunk = max(1, (1 << 26) // (d * 8))
+    for k in range(lo // chunk, (hi + chunk - 1) // chunk):
+        a, b = k * chunk, min(n, (k + 1) * chunk)
+        gk = torch.Generator(device=device)
+        gk.manual_seed(seed * 1_000_003 + k + 1)
+        z = torch.randn(b - a, d, generator=gk, device=device, dtype=torch.float64) / math.sqrt(d)
         z += c * mu
         z /= z.norm(dim=1, keepdim=True)
-        X[i:i + m] = z.to(dtype)
+        s0, s1 = max(a, lo), min(b, hi)
+        if s1 > s0:
+            X[s0 - lo:s1 - lo] = z[s0 - a:s1 - a].to(dtype)
     return X, mu
