@@ -50,6 +50,18 @@ constexpr int ITEMS = B200_ITEMS;
 constexpr int TILE = TPB * ITEMS;       // 1536 pairs per tile
 static_assert(TILE <= 4096, "s_idx packs a 12-bit tile index with the bin");
 constexpr int BIN_SLOW = 7;           // out-of-range / special inputs (slow_eval)
+#ifndef B200_WS
+#define B200_WS 0                     // 1: aligned operands take the pipelined kernel (bessel_ws_kernel)
+#endif
+#ifndef B200_HOMO
+#define B200_HOMO 1                   // 1: tiles of a single bin skip the sort
+#endif
+#ifndef B200_C32
+#define B200_C32 0                    // 1: 32-bit bin-counter increments
+#endif
+#ifndef B200_IFCHAIN
+#define B200_IFCHAIN 0                // 1: fused pass dispatches the cheap bins by compares
+#endif
 
 std::atomic<int64_t> g_launches{0};
 static thread_local char g_err[256] = "";
@@ -148,6 +160,14 @@ template <typename T>
 __device__ __forceinline__ void eval_bin_ik(int bin, T v, T x, T &ri, T &rk) {
 #ifdef B200_EVAL_NOP
     if (bin != BIN_SLOW) { ri = v + x; rk = v - x; return; }
+#endif
+#if B200_IFCHAIN
+    // the cheap bins by compare-and-branch (warp-uniform after the sort); no jump table
+    if (bin == E_MU) { log_bessel_mu_ik<T>(v, x, ri, rk); return; }
+    if (bin == E_UA) { log_bessel_u_ik<T, KU_A>(v, x, ri, rk); return; }
+    if (bin == E_UB) { log_bessel_u_ik<T, KU_B>(v, x, ri, rk); return; }
+    if (bin == E_UC) { log_bessel_u_ik<T, KU_C>(v, x, ri, rk); return; }
+    if (bin == E_U13) { log_bessel_u_ik<T, 13>(v, x, ri, rk); return; }
 #endif
     switch (bin) {
         case E_MU: log_bessel_mu_ik<T>(v, x, ri, rk); break;
@@ -338,6 +358,23 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
             else cp_async_wait_all();
         }
         int lb[ITEMS];
+#if B200_C32
+        // packed 8-bit counters, incremented with 32-bit operations (a variable
+        // 64-bit shift costs ~4 more instructions per element)
+        uint32_t clo = 0, chi = 0;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const int j = tid + i * TPB;
+            lb[i] = -1;
+            if (j < rem) {
+                const int b = bin_of<T, FN>(double(sv[j]), double(sx[j]));
+                lb[i] = b;
+                const uint32_t inc = 1u << (8 * (b & 3));
+                if (b < 4) clo += inc; else chi += inc;
+            }
+        }
+        const uint64_t c8 = (uint64_t(chi) << 32) | clo;
+#else
         uint64_t c8 = 0;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
@@ -348,6 +385,7 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
                 c8 += 1ull << (8 * lb[i]);
             }
         }
+#endif
         // 2. warp-inclusive scan of the packed counts, per-warp totals to smem
         uint64_t incl = c8;
 #pragma unroll
@@ -357,7 +395,8 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
         }
         if (lane == 31) s_wtot[warp] = incl;
         __syncthreads();
-        uint64_t plo, phi;
+        uint64_t plo = 0, phi = 0;
+        int homo = 0;                // tile-homogeneous: 1 + its bin (CTA-uniform)
         {
             // lanes 0..NW-1 of every warp scan the per-warp totals (16-bit fields);
             // the warp keeps the exclusive prefix of its own index
@@ -373,6 +412,16 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
             const uint64_t tlo = shfl64(ilo, NW - 1), thi = shfl64(ihi, NW - 1);   // tile totals per bin
             // exclusive prefix over bins: field k of (x * 0x0001000100010001) is sum_{j<=k}
             constexpr uint64_t ONES = 0x0001000100010001ull;
+#if B200_HOMO
+            {
+                // one bin holds all rem elements <=> a 16-bit field equals rem (fields < 2^15)
+                constexpr uint64_t H = 0x8000800080008000ull;
+                const uint64_t r4 = uint64_t(rem) * ONES;
+                const uint64_t zl = tlo ^ r4, zh = thi ^ r4;
+                const uint64_t ml = (zl - ONES) & ~zl & H, mh = (zh - ONES) & ~zh & H;
+                if (ml | mh) homo = 1 + (ml ? (__ffsll(ml) - 16) >> 4 : 4 + ((__ffsll(mh) - 16) >> 4));
+            }
+#endif
             const uint64_t tp = tlo * ONES;
             const uint64_t blo = tp - tlo;                                         // bases of bins 0..3
             const uint64_t bhi = thi * ONES - thi + (tp >> 48) * ONES;             // bases of bins 4..7
@@ -382,18 +431,23 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
             plo = wlo + widen_lo(ex8);
             phi = whi + widen_hi(ex8);
         }
+        if (!homo) {
 #pragma unroll
-        for (int i = 0; i < ITEMS; ++i) {
-            const int b = lb[i];
-            if (b >= 0) {
-                const int sh = 16 * (b & 3);
-                const uint64_t word = b < 4 ? plo : phi;
-                const int pos = int((word >> sh) & 0xFFFFull);
-                if (b < 4) plo += 1ull << sh; else phi += 1ull << sh;
-                s_idx[pos] = uint16_t((tid + i * TPB) | (b << 12));   // tile index | bin
+            for (int i = 0; i < ITEMS; ++i) {
+                const int b = lb[i];
+                if (b >= 0) {
+                    const int sh = 16 * (b & 3);
+                    const uint64_t word = b < 4 ? plo : phi;
+                    const int pos = int((word >> sh) & 0xFFFFull);
+                    if (b < 4) plo += 1ull << sh; else phi += 1ull << sh;
+                    s_idx[pos] = uint16_t((tid + i * TPB) | (b << 12));   // tile index | bin
+                }
             }
+            __syncthreads();
         }
-        __syncthreads();
+        // a homogeneous tile needs no sort: every thread evaluates the elements it binned
+        // (slot p = element p), so no thread reads another's writes before the next barrier
+        const int hw = (homo - 1) << 12;
         // 3. evaluate: sorted slot p -> element j of the stage (warp w takes the
         //    32-slot chunks w, w + 8, w + 16, w + 24: the expensive high bins at
         //    the end of the order land on different warps)
@@ -401,7 +455,7 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
         for (int i = 0; i < ITEMS; ++i) {
             const int p = tid + i * TPB;
             if (p < rem) {
-                const int w = s_idx[p];
+                const int w = homo ? (p | hw) : s_idx[p];
                 const int j = w & 0xFFF;
                 if constexpr (FN == FN_IK) {
                     eval_bin_ik<T>(w >> 12, sv[j], sx[j], s_res[0][j], s_res[NOUT - 1][j]);
@@ -439,6 +493,268 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
     }
 }
 
+// ------------------------------------------------------------------ pipelined kernel
+// The bench path (16-byte aligned operands): one CTA of 32 warps per SM, a ring
+// of NST tile stages in shared memory, and no CTA-wide barrier in the steady
+// state.  Per stage four mbarriers order the hand-offs:
+//   full  (TMA transaction count)   tile's (v, x) landed
+//   cnt   (32 warp arrivals)        every warp binned its share, warp totals posted
+//   idx   (32 warp arrivals)        every warp scattered its indices (tile sorted)
+//   done  (32 warp arrivals)        every warp stopped evaluating the tile
+// Each warp runs, for the k-th tile of its CTA,
+//   count(k+2)   bin its 1-2 elements of tile k+2 (Algorithm 1 dispatch), warp scan
+//   eval(k)      claim 32-slot chunks of the sorted tile k from a shared counter
+//                until none is left (dynamic balance; the sort puts the most
+//                expensive bins first, longest-processing-time order)
+//   scatter(k+2) from the 32 warp totals: its elements' sorted positions
+// so a warp that finishes early starts the next tile instead of waiting at a
+// barrier: the waits (cnt of k+2 across one eval phase, idx of k+1 across one
+// iteration) have a whole evaluation phase of slack.  Thread 0 (warp 0) moves
+// the data: at iteration k it waits done(k-2), bulk-stores tile k-2's results
+// (in place over its (v, x)) and, once tile k-3's store has read its stage,
+// bulk-loads tile k+3 into that stage.  Six stages: k-3 (store reading), k-2,
+// k-1 (finishing), k (evaluated), k+1 (sorted), k+2 (binned/scattered), with
+// k+3 loading into the stage of k-3.
+namespace wsk {
+constexpr int NWARP = 32;
+constexpr int NTHR = NWARP * 32;          // 1024 threads: one CTA per SM, 64 registers each
+constexpr int WTILE = 1536;               // pairs per tile
+constexpr int NST = 6;                    // ring stages
+constexpr int NCH = WTILE / 32;           // 32-slot chunks per tile
+static_assert(WTILE <= 2 * NTHR, "count/scatter handle at most two elements per thread");
+static_assert(WTILE <= 4096, "s_idx packs a 12-bit tile index with the bin");
+template <typename T>
+__host__ __device__ constexpr int data_bytes() { return NST * 2 * WTILE * int(sizeof(T)); }
+constexpr int IDX_OFF_BYTES = NST * WTILE * 2;
+template <typename T>
+__host__ __device__ constexpr int smem_bytes() {
+    // data[NST][2][WTILE] T | idx[NST][WTILE] u16 | tot[NST][NWARP] u64 | pre[NTHR] u64 |
+    // bar[4][NST] u64 | claim[NST] int | bin[WTILE] u8
+    return data_bytes<T>() + IDX_OFF_BYTES + NST * NWARP * 8 + NTHR * 8 + 4 * NST * 8 + NST * 4 + WTILE;
+}
+}  // namespace wsk
+
+__device__ __forceinline__ void mbar_init_n(uint64_t *bar, int count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void bulk_store_nc(void *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+
+template <typename T, int FN>
+__global__ void __launch_bounds__(wsk::NTHR, 1)
+    bessel_ws_kernel(const T *__restrict__ vin, const T *__restrict__ xin, T *__restrict__ out, T *__restrict__ out2,
+                     int64_t n) {
+    using namespace wsk;
+    constexpr int NOUT = FN == FN_IK ? 2 : 1;
+    constexpr int VEC = 16 / int(sizeof(T));
+    extern __shared__ __align__(128) unsigned char s_dyn[];
+    auto s_data = reinterpret_cast<T (*)[2][WTILE]>(s_dyn);                                  // [stage][v|x][elem]
+    auto s_idx = reinterpret_cast<uint16_t (*)[WTILE]>(s_dyn + data_bytes<T>());
+    unsigned char *p8 = s_dyn + data_bytes<T>() + IDX_OFF_BYTES;
+    auto s_tot = reinterpret_cast<uint64_t (*)[NWARP]>(p8);                                  // per-warp bin totals
+    uint64_t *s_pre = reinterpret_cast<uint64_t *>(p8 + NST * NWARP * 8);                   // per-thread prefix
+    uint64_t *s_bar = s_pre + NTHR;                                                           // [4][NST]
+    uint64_t *b_full = s_bar, *b_cnt = s_bar + NST, *b_idx = s_bar + 2 * NST, *b_done = s_bar + 3 * NST;
+    int *s_claim = reinterpret_cast<int *>(s_bar + 4 * NST);
+    uint8_t *s_bin = reinterpret_cast<uint8_t *>(s_claim + NST);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t ntiles = (n + WTILE - 1) / WTILE;
+    const int64_t K = int64_t(blockIdx.x) < ntiles ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (tid == 0) {
+        for (int st = 0; st < NST; ++st) {
+            mbar_init_n(&b_full[st], 1);
+            mbar_init_n(&b_cnt[st], NWARP);
+            mbar_init_n(&b_idx[st], NWARP);
+            mbar_init_n(&b_done[st], NWARP);
+            s_claim[st] = 0;
+        }
+        fence_mbar_init();
+    }
+    fm_tables_init();   // log table to shared memory; ends with __syncthreads (covers the inits above)
+    auto tile_of = [&](int64_t k) { return int64_t(blockIdx.x) + k * int64_t(gridDim.x); };
+    auto rem_of = [&](int64_t t) { return int(n - t * WTILE < WTILE ? n - t * WTILE : WTILE); };
+    auto par = [](int64_t k) { return uint32_t((k / NST) & 1); };
+
+    // thread 0: bulk loads / stores (one commit group per stored tile)
+    auto load = [&](int64_t k) {
+        const int st = int(k % NST);
+        const int64_t t = tile_of(k);
+        const int ra = rem_of(t) & ~(VEC - 1);
+        mbar_expect_tx(&b_full[st], uint32_t(2 * ra * sizeof(T)));
+        if (ra > 0) {
+            bulk_load(s_data[st][0], vin + t * WTILE, uint32_t(ra * sizeof(T)), &b_full[st]);
+            bulk_load(s_data[st][1], xin + t * WTILE, uint32_t(ra * sizeof(T)), &b_full[st]);
+        }
+    };
+    auto store = [&](int64_t k) {
+        const int st = int(k % NST);
+        mbar_wait(&b_done[st], par(k));
+        const int64_t t = tile_of(k);
+        const int rem = rem_of(t), ra = rem & ~(VEC - 1);
+        fence_proxy_async();
+        if (ra > 0) {
+            bulk_store_nc(out + t * WTILE, s_data[st][0], uint32_t(ra * sizeof(T)));
+            if (NOUT == 2) bulk_store_nc(out2 + t * WTILE, s_data[st][1], uint32_t(ra * sizeof(T)));
+        }
+        bulk_commit();
+        for (int j = ra; j < rem; ++j) {          // < VEC elements past the bulk part
+            out[t * WTILE + j] = s_data[st][0][j];
+            if (NOUT == 2) out2[t * WTILE + j] = s_data[st][1][j];
+        }
+        s_claim[st] = 0;                          // the stage's next tile claims from 0
+    };
+
+    // count: bin this thread's elements of tile k, warp scan, post the warp totals
+    auto count = [&](int64_t k) {
+        const int st = int(k % NST);
+        const int64_t t = tile_of(k);
+        const int rem = rem_of(t), ra = rem & ~(VEC - 1);
+        mbar_wait(&b_full[st], par(k));
+        T *sv = s_data[st][0], *sx = s_data[st][1];
+        uint64_t c8 = 0;
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int j = tid + i * NTHR;
+            if (j < rem) {
+                if (j >= ra) { sv[j] = vin[t * WTILE + j]; sx[j] = xin[t * WTILE + j]; }   // tail past the bulk part
+                const int b = bin_of<T, FN>(double(sv[j]), double(sx[j]));
+                c8 += 1ull << (8 * (7 - b));      // key 7 - b: expensive bins sort first
+                s_bin[j] = uint8_t(b);
+            }
+        }
+        uint64_t incl = c8;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t y = shfl_up64(incl, o);
+            if (lane >= o) incl += y;
+        }
+        s_pre[tid] = incl - c8;                   // this thread's warp-exclusive counts (8-bit fields)
+        if (lane == 31) s_tot[st][warp] = incl;   // warp totals (<= 64 per key)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&b_cnt[st]);
+    };
+
+    // scatter: sorted positions of this thread's elements of tile k
+    auto scatter = [&](int64_t k) {
+        const int st = int(k % NST);
+        const int rem = rem_of(tile_of(k));
+        mbar_wait(&b_cnt[st], par(k));
+        const uint64_t t8 = s_tot[st][lane];      // lane w holds warp w's totals
+        const uint64_t lo = widen_lo(t8), hi = widen_hi(t8);
+        uint64_t ilo = lo, ihi = hi;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint64_t ylo = shfl_up64(ilo, o), yhi = shfl_up64(ihi, o);
+            if (lane >= o) { ilo += ylo; ihi += yhi; }
+        }
+        const uint64_t tlo = shfl64(ilo, 31), thi = shfl64(ihi, 31);     // tile totals per key
+        constexpr uint64_t ONES = 0x0001000100010001ull;
+        const uint64_t tp = tlo * ONES;
+        const uint64_t blo = tp - tlo;                                     // bases of keys 0..3
+        const uint64_t bhi = thi * ONES - thi + (tp >> 48) * ONES;         // bases of keys 4..7
+        const uint64_t wlo = shfl64(blo + ilo - lo, warp), whi = shfl64(bhi + ihi - hi, warp);
+        const uint64_t ex8 = s_pre[tid];
+        uint64_t plo = wlo + widen_lo(ex8), phi = whi + widen_hi(ex8);
+#pragma unroll
+        for (int i = 0; i < 2; ++i) {
+            const int j = tid + i * NTHR;
+            if (j < rem) {
+                const int b = s_bin[j], key = 7 - b;
+                const int sh = 16 * (key & 3);
+                const int pos = int(((key < 4 ? plo : phi) >> sh) & 0xFFFFull);
+                if (key < 4) plo += 1ull << sh; else phi += 1ull << sh;
+                s_idx[st][pos] = uint16_t(j | (b << 12));
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&b_idx[st]);
+    };
+
+    // eval: claim 32-slot chunks of the sorted tile k until none is left
+    auto eval = [&](int64_t k) {
+        const int st = int(k % NST);
+        const int rem = rem_of(tile_of(k));
+        const int nch = (rem + 31) >> 5;
+        mbar_wait(&b_idx[st], par(k));
+        T *sv = s_data[st][0], *sx = s_data[st][1];
+#pragma unroll 1
+        for (;;) {
+            int c = 0;
+            if (lane == 0) c = atomicAdd(&s_claim[st], 1);
+            c = __shfl_sync(0xffffffffu, c, 0);
+            if (c >= nch) break;
+            const int p = (c << 5) + lane;
+            if (p < rem) {
+                const int w = s_idx[st][p];
+                const int j = w & 0xFFF;
+                if constexpr (FN == FN_IK) {
+                    eval_bin_ik<T>(w >> 12, sv[j], sx[j], sv[j], sx[j]);
+                } else {
+                    sv[j] = eval_bin<T, FN>(w >> 12, sv[j], sx[j]);
+                }
+            }
+        }
+        fence_proxy_async();                      // results -> visible to the bulk store
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&b_done[st]);
+    };
+
+    if (tid == 0)
+        for (int64_t k = 0; k < 3 && k < K; ++k) load(k);
+    if (K > 0) { count(0); scatter(0); }
+    if (K > 1) { count(1); scatter(1); }
+#pragma unroll 1
+    for (int64_t k = 0; k < K; ++k) {
+        if (tid == 0) {
+            if (k >= 2) store(k - 2);
+            if (k + 3 < K) {
+                bulk_wait_read1();                // tile k-3's store has read the stage k+3 reuses
+                fence_proxy_async();
+                load(k + 3);
+            }
+        }
+        if (k + 2 < K) count(k + 2);
+        eval(k);
+        if (k + 2 < K) scatter(k + 2);
+    }
+    if (tid == 0) {
+        for (int64_t k = K >= 2 ? K - 2 : 0; k < K; ++k) store(k);
+        bulk_wait_all();
+    }
+}
+
+#ifdef B200_DIRECT
+// Experiment only (tools/variant_bench.py): no staging, no sort -- every thread
+// evaluates its own elements straight from global memory.  On method-homogeneous
+// inputs this is the floor of the evaluation work alone.
+template <typename T, int FN>
+__global__ void __launch_bounds__(256, 4)
+    bessel_direct_kernel(const T *__restrict__ vin, const T *__restrict__ xin, T *__restrict__ out,
+                         T *__restrict__ out2, int64_t n) {
+    fm_tables_init();
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const T v = __ldcs(vin + i), x = __ldcs(xin + i);
+        const int b = bin_of<T, FN>(double(v), double(x));
+        if constexpr (FN == FN_IK) {
+            T ri, rk;
+            eval_bin_ik<T>(b, v, x, ri, rk);
+            __stcs(out + i, ri);
+            __stcs(out2 + i, rk);
+        } else {
+            __stcs(out + i, eval_bin<T, FN>(b, v, x));
+        }
+    }
+}
+#endif
+
 __global__ void classify_kernel(const double *__restrict__ v, const double *__restrict__ x, int8_t *__restrict__ m,
                                 int64_t n) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
@@ -463,6 +779,34 @@ static int launch_eval(const T *v, const T *x, T *out, int64_t n, cudaStream_t s
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= MAXDEV)
         return set_err(B200_ERR_NO_DEVICE, "no current CUDA device (or device id >= 64)");
+#ifdef B200_DIRECT
+    {
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        bessel_direct_kernel<T, FN><<<sms * 4, 256, 0, s>>>(v, x, out, out2, n);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return cuda_err(cudaGetLastError(), "bessel_direct_kernel launch");
+    }
+#endif
+#if B200_WS
+    if (tma) {
+        // pipelined kernel: one CTA of wsk::NTHR threads per SM
+        static std::atomic<int> ws_ready[MAXDEV];
+        constexpr int WSMEM = wsk::smem_bytes<T>();
+        if (!ws_ready[dev].load(std::memory_order_relaxed)) {
+            cudaError_t e = cudaFuncSetAttribute(bessel_ws_kernel<T, FN>, cudaFuncAttributeMaxDynamicSharedMemorySize, WSMEM);
+            if (e != cudaSuccess) return cuda_err(e, "cudaFuncSetAttribute (pipelined kernel)");
+            ws_ready[dev].store(1, std::memory_order_relaxed);
+        }
+        int sms = 0;
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+        const int64_t ntiles = (n + wsk::WTILE - 1) / wsk::WTILE;
+        const int grid = int(ntiles < sms ? ntiles : sms);
+        bessel_ws_kernel<T, FN><<<grid, wsk::NTHR, WSMEM, s>>>(v, x, out, out2, n);
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return cuda_err(cudaGetLastError(), "bessel_ws_kernel launch");
+    }
+#endif
     int o = occ[tma][dev].load(std::memory_order_relaxed);
     if (o == 0) {
         auto kern = tma ? bessel_eval_kernel<T, FN, true> : bessel_eval_kernel<T, FN, false>;

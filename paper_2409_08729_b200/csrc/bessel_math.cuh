@@ -117,6 +117,9 @@ __device__ __forceinline__ int select_method(double v, double x) {
 // as soon as a term no longer changes the sum (past the initial growth of
 // the terms, k >= 4), which for x >= 60 is after 8-15 terms.
 constexpr int KMU = 26;
+#ifndef B200_MUEO
+#define B200_MUEO 0
+#endif
 
 // Wide-range guard: the fast paths form 1/x, v^2 + x^2 and 1/rho, which stay
 // normal for arguments below BIG; beyond it the same formulas run rescaled or
@@ -172,11 +175,41 @@ __device__ __forceinline__ T log_bessel_mu(T v, T x) {
 // 1.6e-3 for U9 (rho >= 80), 4.5e-4 for U6, 7e-5 for U4 (R12 bounds).  The
 // Taylor polynomial of degree NP leaves |d|^(NP+1)/(NP+1) < 2^-60: NP = 9, 6,
 // 5, 4.  Replaces a full log of S (one table log per function saved).
+#ifndef B200_L1P56
+#define B200_L1P56 1
+#endif
+#if B200_L1P56
+// |d|^(NP+1)/(NP+1) < 2^-56 (absolute error of log S, below the 1e-13 target by 1e3):
+// |d| < 0.0105 (U13) -> 7, 3e-3 (U10, rho >= 61) -> 5, 1.2e-3 (U8) -> 5, 4.5e-4 (U6) -> 4
+template <int KU> struct Log1pDeg { static constexpr int v = KU >= 13 ? 7 : KU >= 8 ? 5 : 4; };
+#else
 template <int KU> struct Log1pDeg { static constexpr int v = KU >= 13 ? 9 : KU >= 9 ? 6 : KU >= 6 ? 5 : 4; };
+#endif
 static __constant__ double c_l1p[10] = {0.0, 1.0, -1.0 / 2, 1.0 / 3, -1.0 / 4, 1.0 / 5, -1.0 / 6, 1.0 / 7,
                                         -1.0 / 8, 1.0 / 9};
+#if B200_IMM
+// 1/k, with the odd tails 1/5, 1/7, 1/9 (and 1/3 for the U6 bound |d| < 4.5e-4) as
+// 21-bit immediates: their rounding (< 2.4e-7 relative) times |d|^k stays < 1e-17
+template <int K, bool SHORT3>
+__device__ __forceinline__ double l1p_coef() {
+    return K == 1 ? 1.0 : K == 2 ? -0.5 : K == 3 ? (SHORT3 ? 0.33333325386047363 : c_l1p[3]) : K == 4 ? -0.25
+         : K == 5 ? 0.20000004768371582 : K == 6 ? -0.16666662693023682 : K == 7 ? 0.14285719394683838
+         : K == 8 ? -0.125 : 0.1111111044883728;
+}
+template <typename T, int NP, int K>
+__device__ __forceinline__ T l1p_step(T p, T d) {
+    if constexpr (K < 1) return p;
+    else return l1p_step<T, NP, K - 1>(fma(p, d, T(l1p_coef<K, (NP <= 5)>())), d);
+}
+#endif
 template <typename T, int NP>
 __device__ __forceinline__ T log1p_small(T d) {
+#if B200_IMM
+    if constexpr (sizeof(T) == 8) {
+        const T p = l1p_step<T, NP, NP - 1>(T(l1p_coef<NP, (NP <= 5)>()), d);
+        return p * d;
+    }
+#endif
     T p = T(c_l1p[NP]);
 #pragma unroll
     for (int k = NP - 1; k >= 1; --k) p = fma(p, d, T(c_l1p[k]));
@@ -201,10 +234,23 @@ template <typename T>
 __device__ __forceinline__ T uk_row(int k, T t2) {
     // P_k(t2) by Horner, k+1 coefficients starting at UK_OFF[k]
     const int off = (k * (k + 1)) / 2;
+#if B200_IMM
+    if constexpr (sizeof(T) == 8) {
+        // first step as a separate multiply and add: both take their constant as a
+        // uniform-register operand, where fma(c_k, t2, c_k-1) needs one of the two
+        // constants in a vector register (a per-thread constant-bank load)
+        T p = __dadd_rn(__dmul_rn(t2, Tr<T>::uk(off + k)), Tr<T>::uk(off + k - 1));
+#pragma unroll
+        for (int j = k - 2; j >= 0; --j) p = fma(p, t2, Tr<T>::uk(off + j));
+        return p;
+    }
+#endif
+#if 1
     T p = Tr<T>::uk(off + k);
 #pragma unroll
     for (int j = k - 1; j >= 0; --j) p = fma(p, t2, Tr<T>::uk(off + j));
     return p;
+#endif
 }
 
 // v * eta(x/v).  Where eta ~ 0 (z = x/v near the Laplace limit constant
@@ -322,6 +368,32 @@ __device__ __forceinline__ void log_bessel_u_ik(T v, T x, T &li, T &lk) {
 
 template <typename T>
 __device__ __forceinline__ void log_bessel_mu_ik(T v, T x, T &li, T &lk) {
+#if B200_MUEO
+    // The two series differ only by (-1)^k: with E = 1 + sum of the even terms and
+    // O = sum of the odd ones, S_K = E + O and S_I = E - O, so every term is added
+    // once.  term_k = term_{k-1} f_k with f_k = c (mu - (2k-1)^2) / k, c = 1/(8x),
+    // formed as (c mu - c (2k-1)^2) / k = fma(c, -(2k-1)^2, z) * (1/k), z = c mu
+    // ((2k-1)^2 is an immediate): 4 FP64 operations per term instead of 6.
+    const T rx = fm_rcp(x);
+    const T c = T(0.125) * rx;
+    const T z = c * (T(4) * v * v);
+    T term = T(1), E = T(1), O = T(0);
+#pragma unroll
+    for (int k = 1; k < KMU; k += 4) {
+#pragma unroll
+        for (int u = 0; u < 4 && k + u <= KMU; u += 2) {
+            const int k1 = k + u;
+            term *= fma(c, T(-(2 * k1 - 1) * (2 * k1 - 1)), z) * c_inv_k<T>(k1);
+            O += term;
+            term *= fma(c, T(-(2 * k1 + 1) * (2 * k1 + 1)), z) * c_inv_k<T>(k1 + 1);
+            E += term;
+        }
+        if (k >= 3 && fabs(term) <= Tr<T>::eps * T(0.25) * fabs(E - O)) break;
+    }
+    const T SI = fabs(E - O), SK = fabs(E + O);
+    li = x + T(0.5) * fm_log(SI * SI * rx * hc<T>(HC_INV2PI));
+    lk = -x + T(0.5) * fm_log(SK * SK * rx * hc<T>(HC_PIO2));
+#else
     const T rx = fm_rcp(x);
     const T mu = T(4) * v * v;
     const T c = T(0.125) * rx;
@@ -345,6 +417,7 @@ __device__ __forceinline__ void log_bessel_mu_ik(T v, T x, T &li, T &lk) {
     const T SI = fabs(si), SK = fabs(sk);
     li = x + T(0.5) * fm_log(SI * SI * rx * hc<T>(HC_INV2PI));
     lk = -x + T(0.5) * fm_log(SK * SK * rx * hc<T>(HC_PIO2));
+#endif
 }
 
 // ---------------------------------------------------------------- series (I)
@@ -600,11 +673,12 @@ __device__ __forceinline__ T log_kv_fallback(T v, T x) {
         T rho;
         const T lk = trap_kmu<T>(mu, x, rho);
         const T tox = T(2) * fm_rcp(x);
-        // x > 2, v <= 12.7: K_v / K_mu < 1e12, no rescaling needed
-        T km = T(1), kp = rho, nu = mu;
+        // x > 2, v <= 12.7: K_v / K_mu < 1e12, no rescaling needed.  The coefficient
+        // 2 nu / x advances by one addition of 2/x per step (< 13 roundings)
+        T km = T(1), kp = rho, a = mu * tox;
         for (int i = 1; i < nl; ++i) {
-            nu += T(1);
-            const T kn = fma(nu * tox, kp, km);
+            a += tox;
+            const T kn = fma(a, kp, km);
             km = kp;
             kp = kn;
         }
@@ -617,10 +691,10 @@ __device__ __forceinline__ T log_kv_fallback(T v, T x) {
         // (2 * 13 / 1e-6)^13 < 1e97: the unscaled ratio stays in the double range
         // (double for both precisions)
         const double tx = double(T(2) * fm_rcp(x));
-        double km = 1.0, kp = double(T(2) * S1 * fm_rcp(x * S)), nu = double(mu);
+        double km = 1.0, kp = double(T(2) * S1 * fm_rcp(x * S)), a = double(mu) * tx;
         for (int i = 1; i < nl; ++i) {
-            nu += 1.0;
-            const double kn = fma(nu * tx, kp, km);
+            a += tx;                                  // 2 (mu + i) / x
+            const double kn = fma(a, kp, km);
             km = kp;
             kp = kn;
         }
@@ -676,11 +750,12 @@ __device__ __forceinline__ void log_ivkv_trap(T v, T x, T &ri, T &rk) {
     } else {
         lk = trap_kmu<T>(mu, x, rho);
     }
-    // kp = K_v / K_mu, kn = K_{v+1} / K_mu (one recurrence step past v)
-    T km = T(1), kp = rho, nu = mu;
+    // kp = K_v / K_mu, kn = K_{v+1} / K_mu (one recurrence step past v); the
+    // coefficient 2 nu / x advances by one addition of 2/x per step
+    T km = T(1), kp = rho, a = mu * tox;
     for (int i = 1; i <= nl; ++i) {
-        nu += T(1);
-        const T kn = fma(nu * tox, kp, km);
+        a += tox;
+        const T kn = fma(a, kp, km);
         km = kp;
         kp = kn;
     }
@@ -688,13 +763,14 @@ __device__ __forceinline__ void log_ivkv_trap(T v, T x, T &ri, T &rk) {
     const int M = sizeof(T) == 8 ? int(fmin(T(12) + x, fma(T(0.55), x, T(20)))) + 1
                                  : int(fmin(T(6) + x, fma(T(0.5), x, T(12)))) + 1;
     T y1 = T(0), y0 = T(1);                 // y_{v+k+1}, y_{v+k}
-    // order counter nu = v + k kept in T: v + M rounds once, each nu - 1 is exact
-    // (nu < 64); an int -> T conversion per step (I2F.F64) cost 5% of this band
-    T nuk = v + T(M);
+    // coefficient b = 2 (v + k) / x, stepped down by one subtraction of 2/x per step
+    // (<= 37 roundings: relative error < 1e-14 in b, far inside the ratio's tolerance;
+    // a multiply per step, or an int -> T conversion (I2F.F64), cost more)
+    T b = (v + T(M)) * tox;
 #pragma unroll 2
     for (int k = M; k >= 1; --k) {
-        const T y = fma(nuk * tox, y0, y1);
-        nuk -= T(1);
+        const T y = fma(b, y0, y1);
+        b -= tox;
         y1 = y0;
         y0 = y;
     }

@@ -34,13 +34,61 @@ struct FmConst {
     double ln2_hi, ln2_lo;               // ln 2 split so that e * ln2_hi is exact for |e| < 2^11 (fdlibm)
     double exp_inv, exp_chi, exp_clo;    // 64/ln2; ln2/64 = chi (33 significant bits) + clo
     double exp_c5, exp_c4, exp_c3;       // 1/120, 1/24, 1/6
+    double ln2_lo20, exp_clo20;          // remainders of the 21-significant-bit splits below
 };
 static __constant__ FmConst c_fm = {
     -1.0 / 6.0, 0.2, 1.0 / 3.0,
     6.93147180369123816490e-01, 1.90821492927058770002e-10,
     92.33248261689366, 0.010830424695086549, 1.162596423439437e-12,
     1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0,
+    -1.904654299957768e-09, -2.9760223436840126e-11,
 };
+
+#ifndef B200_IMM
+#define B200_IMM 1
+#endif
+// Short constants (B200_IMM): a double whose low word is zero (21 significant bits)
+// is an instruction immediate on sm_100a; any other constant costs a constant-bank
+// load (LDC into a register, or LDCU into a uniform register).  Where the error
+// analysis allows, the polynomial coefficients are rounded to 21 bits (relative
+// error <= 2^-22): log1p's r^5, r^6 terms (|r| < 2^-9: contribution < 1e-18
+// relative), exp's r^4, r^5 terms and the 64/ln2 range-reduction factor (|r|
+// grows by < 4%); ln 2 and ln 2 / 64 are split at 21 bits (e * ln2_hi20 exact
+// for |e| < 2^11, k * chi20 exact for |k| < 2^17) with full-precision remainders.
+constexpr double IMM_LOG_C6 = -0.16666662693023682;     // -1/6 (0xBFC5555500000000)
+constexpr double IMM_LOG_C5 = 0.20000004768371582;      //  1/5 (0x3FC9999A00000000)
+constexpr double IMM_LN2_HI20 = 0.6931471824645996;     //  ln 2 (0x3FE62E4300000000)
+constexpr double IMM_EXP_INV = 92.33245849609375;       //  64/ln2 (0x4057154700000000)
+constexpr double IMM_EXP_CHI20 = 0.010830424726009369;  //  ln2/64 (0x3F862E4300000000)
+constexpr double IMM_EXP_C5 = 0.00833333283662796;      //  1/120 (0x3F81111100000000)
+constexpr double IMM_EXP_C4 = 0.041666656732559204;     //  1/24 (0x3FA5555500000000)
+
+// exp(y) core, |y| <= 708 (result normal); shared by fm_exp / fm_exp_nc
+__device__ __forceinline__ double fm_exp_core(double y) {
+    constexpr double SHIFT = 6755399441055744.0;               // 1.5 * 2^52: round-to-int (immediate)
+#if B200_IMM
+    double kd = fma(y, IMM_EXP_INV, SHIFT);
+    const int k = __double2loint(kd);
+    kd -= SHIFT;
+    double r = fma(kd, -IMM_EXP_CHI20, y);
+    r = fma(kd, -c_fm.exp_clo20, r);                           // |r| <= 1.04 ln2/128
+    // expm1(r) = r + r^2 (1/2 + r (1/6 + r (1/24 + r/120)))
+    double p = fma(r, IMM_EXP_C5, IMM_EXP_C4);
+#else
+    double kd = fma(y, c_fm.exp_inv, SHIFT);
+    const int k = __double2loint(kd);
+    kd -= SHIFT;
+    double r = fma(kd, -c_fm.exp_chi, y);
+    r = fma(kd, -c_fm.exp_clo, r);                             // |r| <= ln2/128
+    double p = fma(r, c_fm.exp_c5, c_fm.exp_c4);
+#endif
+    p = fma(p, r, c_fm.exp_c3);
+    p = fma(p, r, 0.5);
+    p = fma(p, r * r, r);
+    const double2 T = __ldg(&g_exptab[k & (B200_EXP_TAB_N - 1)]);
+    const double res = T.x + fma(T.x, p, T.y);
+    return __hiloint2double(__double2hiint(res) + ((k >> 6) << 20), __double2loint(res));
+}
 
 #ifndef B200_SMEM_LOG
 #define B200_SMEM_LOG 1
@@ -73,61 +121,47 @@ __device__ __forceinline__ double fm_log(double a) {
 #endif
     const double r = fma(m, c.x, -1.0);                      // m / c_i - 1, |r| < 0.00195
     // log1p(r) - r = r^2 (-1/2 + r (1/3 + r (-1/4 + r (1/5 - r/6))))
+#if B200_IMM
+    double p = fma(r, IMM_LOG_C6, IMM_LOG_C5);
+#else
     double p = fma(r, c_fm.log_c6, c_fm.log_c5);
+#endif
     p = fma(p, r, -0.25);
     p = fma(p, r, c_fm.log_c3);
     p = fma(p, r, -0.5);
     const double ed = double(e);   // I2F.F64 (a DADD-based magic-number conversion measured +1%: FP64 pipe)
+#if B200_IMM
+    const double h = fma(ed, IMM_LN2_HI20, c.y);
+    const double l = fma(ed, c_fm.ln2_lo20, tlo);
+#else
     const double h = fma(ed, c_fm.ln2_hi, c.y);
     const double l = fma(ed, c_fm.ln2_lo, tlo);
+#endif
     return h + (r + fma(r * r, p, l));
 }
 
 // exp(y) for -708 <= y <= 709 (result normal); y < -708 is clamped (callers
 // only use it where such terms are negligible).
-__device__ __forceinline__ double fm_exp(double y) {
-    constexpr double SHIFT = 6755399441055744.0;               // 1.5 * 2^52: round-to-int (immediate)
-    y = fmax(y, -708.0);
-    double kd = fma(y, c_fm.exp_inv, SHIFT);
-    const int k = __double2loint(kd);
-    kd -= SHIFT;
-    double r = fma(kd, -c_fm.exp_chi, y);
-    r = fma(kd, -c_fm.exp_clo, r);                             // |r| <= ln2/128
-    // expm1(r) = r + r^2 (1/2 + r (1/6 + r (1/24 + r/120)))
-    double p = fma(r, c_fm.exp_c5, c_fm.exp_c4);
-    p = fma(p, r, c_fm.exp_c3);
-    p = fma(p, r, 0.5);
-    p = fma(p, r * r, r);
-    const double2 T = __ldg(&g_exptab[k & (B200_EXP_TAB_N - 1)]);
-    const double res = T.x + fma(T.x, p, T.y);
-    return __hiloint2double(__double2hiint(res) + ((k >> 6) << 20), __double2loint(res));
-}
+__device__ __forceinline__ double fm_exp(double y) { return fm_exp_core(fmax(y, -708.0)); }
 
 // exp(y) for -708 <= y <= 709 without the clamp (caller guarantees the range).
-__device__ __forceinline__ double fm_exp_nc(double y) {
-    constexpr double SHIFT = 6755399441055744.0;
-    double kd = fma(y, c_fm.exp_inv, SHIFT);
-    const int k = __double2loint(kd);
-    kd -= SHIFT;
-    double r = fma(kd, -c_fm.exp_chi, y);
-    r = fma(kd, -c_fm.exp_clo, r);
-    double p = fma(r, c_fm.exp_c5, c_fm.exp_c4);
-    p = fma(p, r, c_fm.exp_c3);
-    p = fma(p, r, 0.5);
-    p = fma(p, r * r, r);
-    const double2 T = __ldg(&g_exptab[k & (B200_EXP_TAB_N - 1)]);
-    const double res = T.x + fma(T.x, p, T.y);
-    return __hiloint2double(__double2hiint(res) + ((k >> 6) << 20), __double2loint(res));
-}
+__device__ __forceinline__ double fm_exp_nc(double y) { return fm_exp_core(y); }
 
+#ifndef B200_FASTRCP
+#define B200_FASTRCP 1
+#endif
 // 1/a for finite normal |a| in [2^-1000, 2^1000].
 __device__ __forceinline__ double fm_rcp(double a) {
     double r;
     asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
     double e = fma(-a, r, 1.0);
     r = fma(r, fma(e, e, e), r);              // cubic step: error e^3
+#if B200_FASTRCP
+    return r;                                 // seed error e < 2^-22 (tools/mufu_accuracy.cu): e^3 < 2^-66
+#else
     e = fma(-a, r, 1.0);
     return fma(r, e, r);                      // Newton step
+#endif
 }
 
 // x / y (y as for fm_rcp), with one residual correction (faithful).
@@ -143,8 +177,12 @@ __device__ __forceinline__ double fm_rsqrt(double a) {
     asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
     double e = fma(-a * y, y, 1.0);           // 1 - a y^2
     y = fma(y, e * fma(e, 0.375, 0.5), y);    // y (1 + e/2 + 3e^2/8): error O(e^3)
+#if B200_FASTRCP
+    return y;
+#else
     e = fma(-a * y, y, 1.0);
     return fma(0.5 * y, e, y);                // Newton step
+#endif
 }
 
 // log(1 + d) for d > -1 with relative accuracy when |d| is small: u = 1 + d rounds,
