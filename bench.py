@@ -127,6 +127,31 @@ def _fp64_peak():
     return None, None
 
 
+def _fp64_theoretical():
+    """148 SMs x 64 FP64 FMA lanes/clk x 2 flop x the max SM clock (profiles/fp64_peak.json)."""
+    p = os.path.join(ROOT, "profiles", "fp64_peak.json")
+    if os.path.exists(p):
+        return json.load(open(p)).get("theoretical_tflops_at_max_clock")
+    return None
+
+
+def _fn_roofline(name, evals, ms):
+    """FP64 roofline of one single-function launch (flop per evaluation: ncu, profiles/roofline_counts.json)."""
+    cnt = _roofline_counts().get(name, {})
+    peak, src = _fp64_peak()
+    fl = cnt.get("fp64_flop_per_eval")
+    if not fl or not peak or ms <= 0:
+        return None
+    tf = fl * evals / (ms / 1e3) / 1e12
+    hbm_peak, _ = _peaks()
+    gbs = 24 * evals / (ms / 1e3) / 1e9
+    theo = _fp64_theoretical()
+    return {"bound": "alu", "achieved": tf, "peak": peak, "unit": "TFLOP/s", "frac": tf / peak,
+            "frac_vs_theoretical": (tf / theo) if theo else None, "fp64_flop_per_eval": fl,
+            "flop_source": cnt.get("source"), "hbm": {"achieved_gbs": gbs, "frac": gbs / hbm_peak,
+                                                      "algorithmic_bytes_per_eval": 24}}
+
+
 def cpu_baseline(target_s=12.0, seed=123):
     """The oracle (as it stands) on host cores, bounded sample of the same workload."""
     import numpy as np
@@ -255,9 +280,16 @@ def run_extra(args, B, workloads, ws, rank, dev, stream, dist):
     o1, o2 = torch.empty_like(v32), torch.empty_like(v32)
     B.log_ivkv(v32, x32, o1, o2)
     ms = _timed(lambda: B.log_ivkv(v32, x32, o1, o2), 3, stream, dist)
+    hbm_peak, _ = _peaks()
+    gbs32 = 16 * v32.numel() / (ms / 3 / 1e3) / 1e9
     out["fp32_fused"] = {"config": "configs[2] fp32 variant: bench grid in float32, b200_log_ivkv_f32",
                          "value": 2 * v32.numel() * ws * 3 / (ms / 1e3) / 1e9, "unit": UNIT,
-                         "ms_per_step": ms / 3, "dtype": "f32"}
+                         "ms_per_step": ms / 3, "dtype": "f32",
+                         "roofline": {"bound": "hbm", "achieved": gbs32, "peak": hbm_peak, "unit": "GB/s",
+                                      "frac": gbs32 / hbm_peak, "algorithmic_bytes_per_pair": 16,
+                                      "floor_ms": 16 * v32.numel() / (hbm_peak * 1e9) * 1e3,
+                                      "note": "16 B per pair (v, x in; log I, log K out, float32); the f32 "
+                                              "kernel is issue-bound, so this is the distance to the HBM floor"}}
     del v32, x32, o1, o2
     # -- the paper's own runtime table (Table 5): 10M fractional-order
     #    pairs uniform on the Small [0,150]^2 / Large [150,1e4]^2 (I) or [150,4000]^2 (K)
@@ -368,10 +400,13 @@ def run_ours(args):
         ms_sep = _timed(step_sep, args.steps, stream, dist)
         for _ in range(args.steps):
             step_sep_acc()
+        kiv, kkv = acc[0] / args.steps, acc[1] / args.steps
         sep = {"value": evals_per_step * args.steps / (ms_sep / 1e3) / 1e9, "unit": UNIT,
                "ms_per_step": ms_sep / args.steps,
-               "kernel_ms": {"log_iv": acc[0] / args.steps, "log_kv": acc[1] / args.steps},
-               "note": "b200_log_iv_f64 then b200_log_kv_f64 over the same grid (2 launches per step)"}
+               "kernel_ms": {"log_iv": kiv, "log_kv": kkv},
+               "roofline": {"log_iv": _fn_roofline("log_iv", n, kiv), "log_kv": _fn_roofline("log_kv", n, kkv)},
+               "note": "b200_log_iv_f64 then b200_log_kv_f64 over the same grid (2 launches per step); "
+                       "per-function FP64 roofline from CUDA events around each launch"}
 
     # ---- end to end through the C ABI with pinned HOST buffers (H2D + kernel + D2H timed)
     e2e = None
@@ -433,6 +468,10 @@ def run_ours(args):
                     "flop_source": cnt["source"] + " (DADD + DMUL + 2 DFMA executed per pair)",
                     "hbm": {"achieved_gbs": gbs, "peak_gbs": hbm_peak, "frac": gbs / hbm_peak,
                             "algorithmic_bytes_per_pair": BYTES_PER_PAIR}}
+            theo = _fp64_theoretical()
+            if theo:
+                roof["frac_vs_theoretical"] = tf / theo
+                roof["theoretical_peak"] = theo
             fi = cnt.get("fp64_inst_per_eval")
             if fi:
                 # FP64-pipe occupancy view: a DADD or DMUL takes a pipe slot like a DFMA

@@ -92,16 +92,27 @@ enum : int { FN_I = 0, FN_K = 1, FN_K_PAPER = 2, FN_IK = 3 };   // FN_IK: both, 
 // where v^2 + x^2, 1/x, x/(v + rho) and x^2/4 are still normal floats.
 template <typename T> struct Range;
 template <> struct Range<double> { static constexpr uint32_t lo = B200_HW_LO, hi = B200_HW_HI; };
-template <> struct Range<float> { static constexpr uint32_t lo = B200_HW_LO32, hi = B200_HW_HI32; };
+template <> struct Range<float> { static constexpr uint32_t lo = B200_F32_LO32, hi = B200_F32_HI32; };   // float bits
 
 template <typename T, int FN>
-__device__ __forceinline__ int bin_of(double v, double x) {
+__device__ __forceinline__ int bin_of(T v, T x) {
     constexpr uint32_t LO = Range<T>::lo, HI = Range<T>::hi;
-    const uint32_t hx = hiw(x), hvs = hiw(v), hv = hvs & 0x7FFFFFFFu;
+    uint32_t hx, hvs;
+    if constexpr (sizeof(T) == 8) {
+        hx = hiw(x);
+        hvs = hiw(v);
+    } else {                                                            // f32: float bit patterns
+        hx = __float_as_uint(x);
+        hvs = __float_as_uint(v);
+    }
+    const uint32_t hv = hvs & 0x7FFFFFFFu;
     if (hx - LO > HI - LO) return BIN_SLOW;                             // x outside the range (or <= 0, NaN)
     if (hv > HI) return BIN_SLOW;                                       // |v| above the range, inf, NaN
     if ((FN == FN_I || FN == FN_IK) && hvs != hv) return BIN_SLOW;     // v < 0 (or -0.0: handled there)
-    return select_eval_hw(fabs(v), x, hv, hx, (FN == FN_I) ? B200_HW_X8 : B200_HW_X2);
+    if constexpr (sizeof(T) == 8)
+        return select_eval_hw(fabs(v), x, hv, hx, (FN == FN_I) ? B200_HW_X8 : B200_HW_X2);
+    else
+        return select_eval_f32(fabsf(v), x, hv, hx, (FN == FN_I) ? B200_F32_X8 : B200_F32_X2);
 }
 
 // The slow bin: IEEE special cases, then the full-range (SAFE) evaluation.
@@ -367,7 +378,7 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
             const int j = tid + i * TPB;
             lb[i] = -1;
             if (j < rem) {
-                const int b = bin_of<T, FN>(double(sv[j]), double(sx[j]));
+                const int b = bin_of<T, FN>(sv[j], sx[j]);
                 lb[i] = b;
                 const uint32_t inc = 1u << (8 * (b & 3));
                 if (b < 4) clo += inc; else chi += inc;
@@ -381,7 +392,7 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
             const int j = tid + i * TPB;
             lb[i] = -1;
             if (j < rem) {
-                lb[i] = bin_of<T, FN>(double(sv[j]), double(sx[j]));
+                lb[i] = bin_of<T, FN>(sv[j], sx[j]);
                 c8 += 1ull << (8 * lb[i]);
             }
         }
@@ -625,7 +636,7 @@ __global__ void __launch_bounds__(wsk::NTHR, 1)
             const int j = tid + i * NTHR;
             if (j < rem) {
                 if (j >= ra) { sv[j] = vin[t * WTILE + j]; sx[j] = xin[t * WTILE + j]; }   // tail past the bulk part
-                const int b = bin_of<T, FN>(double(sv[j]), double(sx[j]));
+                const int b = bin_of<T, FN>(sv[j], sx[j]);
                 c8 += 1ull << (8 * (7 - b));      // key 7 - b: expensive bins sort first
                 s_bin[j] = uint8_t(b);
             }
@@ -742,7 +753,7 @@ __global__ void __launch_bounds__(256, 4)
     fm_tables_init();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
         const T v = __ldcs(vin + i), x = __ldcs(xin + i);
-        const int b = bin_of<T, FN>(double(v), double(x));
+        const int b = bin_of<T, FN>(v, x);
         if constexpr (FN == FN_IK) {
             T ri, rk;
             eval_bin_ik<T>(b, v, x, ri, rk);

@@ -120,6 +120,9 @@ constexpr int KMU = 26;
 #ifndef B200_MUEO
 #define B200_MUEO 0
 #endif
+#ifndef B200_MUF
+#define B200_MUF 1
+#endif
 
 // Wide-range guard: the fast paths form 1/x, v^2 + x^2 and 1/rho, which stay
 // normal for arguments below BIG; beyond it the same formulas run rescaled or
@@ -293,7 +296,7 @@ __device__ __forceinline__ T v_times_eta(T v, T x, T vs, T xs, T rhos, T rho) {
         return fma(v, lq, rho);
     }
     const T q = xs * fm_rcp(vs + rhos);
-    return fma(v, fm_log(q), rho);
+    return fma(v, fm_log_acc(q), rho);
 }
 
 // Number of U_K terms.  The paper's Table 1 fits regions for U4/U6/U9/U13 and
@@ -398,6 +401,11 @@ __device__ __forceinline__ void log_bessel_mu_ik(T v, T x, T &li, T &lk) {
     const T mu = T(4) * v * v;
     const T c = T(0.125) * rx;
     T term = T(1), si = T(1), sk = T(1);          // K terms (all signs +); I alternates
+#if B200_MUF
+    // factor c (mu - (2k-1)^2) / k formed as fma(c, -(2k-1)^2, c mu) * (1/k): the odd
+    // square is an immediate, one FP64 operation fewer per term than (mu - sq) * (c / k)
+    const T z = c * mu;
+#endif
     // terms in (odd, even) pairs, fully unrolled: (2k-1)^2 and 1/k are constants
 #pragma unroll
     for (int k = 1; k < KMU; k += 4) {         // four terms per stop test (KMU = 4*6 + 2)
@@ -405,10 +413,18 @@ __device__ __forceinline__ void log_bessel_mu_ik(T v, T x, T &li, T &lk) {
         for (int u = 0; u < 4 && k + u <= KMU; u += 2) {
             const int k1 = k + u;
             const T i1 = c_inv_k<T>(k1), i2 = c_inv_k<T>(k1 + 1);
+#if B200_MUF
+            term *= fma(c, T(-(2 * k1 - 1) * (2 * k1 - 1)), z) * i1;
+#else
             term *= (mu - T((2 * k1 - 1) * (2 * k1 - 1))) * (c * i1);
+#endif
             si -= term;                            // summed in order, as the separate
             sk += term;                            // series (no even/odd cancellation)
+#if B200_MUF
+            term *= fma(c, T(-(2 * k1 + 1) * (2 * k1 + 1)), z) * i2;
+#else
             term *= (mu - T((2 * k1 + 1) * (2 * k1 + 1))) * (c * i2);
+#endif
             si += term;
             sk += term;
         }
@@ -849,6 +865,26 @@ __device__ __forceinline__ int select_eval_hw(double v, double x, uint32_t hv, u
 }
 __device__ __forceinline__ int select_eval(double v, double x, uint32_t hw_split) {
     return select_eval_hw(v, x, hiw(v), hiw(x), hw_split);
+}
+
+// The same dispatch on float inputs with float keys (f32 kernels): the keys are the
+// float bit patterns, each "a > C" is bits(a) > bits(C_dn) with C_dn the largest float
+// <= C (exact for float a), each "a >= rho_K" bits(a) >= bits(rho_K) -- no conversion
+// of the inputs to double (tables.h B200_F32_*; R3).
+__device__ __forceinline__ bool mu_edge_f32(float v, float x) {
+    const float d = 0.5113f * __log2f(x) + 1.14535832f - __log2f(v);   // 0.7939 / ln 2
+    if (fabsf(d) > 1e-4f) return d > 0.0f;
+    return 0.5113 * log(double(x)) + 0.7939 > log(double(v));         // guard band: the double predicate
+}
+__device__ __forceinline__ int select_eval_f32(float v, float x, uint32_t hv, uint32_t hx, uint32_t split) {
+    const uint32_t m = hv > hx ? hv : hx;
+    const int eu = m >= B200_CAT(B200_F32_RHO_K, B200_KU_A) ? E_UA : m >= B200_CAT(B200_F32_RHO_K, B200_KU_B) ? E_UB
+                 : m >= B200_CAT(B200_F32_RHO_K, B200_KU_C) ? E_UC : E_U13;
+    const int ef = hx > split ? E_FB_B : E_FB_A;
+    const bool u = (hx > B200_F32_X19 && hv > B200_F32_V07) || hv > B200_F32_V12;
+    bool mu = hx > B200_F32_X30 && hv <= B200_F32_V15;                   // x > 30 && v < 15.3919
+    if (!mu && hx > B200_F32_X59 && hv < hx) mu = (hv == 0) || mu_edge_f32(v, x);
+    return mu ? E_MU : (u ? eu : ef);
 }
 
 template <typename T, bool SAFE>

@@ -193,18 +193,45 @@ __device__ __forceinline__ double fm_log1p(double d) {
     return fm_log(u) - ((u - 1.0) - d) * fm_rcp(u);
 }
 
+__device__ __forceinline__ double fm_log_acc(double a) { return fm_log(a); }
+
 // log(a) for any finite a > 0 (subnormals through the library function).
 __device__ __forceinline__ double fm_log_wide(double a) { return a >= 1e-300 ? fm_log(a) : log(a); }
 
-// f32 path: the CUDA single-precision functions (the MUFU intrinsics
-// __logf/__expf measured no faster here: the f32 kernel is bound by the same
-// tile machinery as the f64 one).
+#ifndef B200_F32FAST
+#define B200_F32FAST 1
+#endif
+// f32 path.  B200_F32FAST: the hardware approximations (MUFU) -- log via lg2.approx
+// (absolute error < 2^-21.4 on [1/2, 2], <= 3 ulp elsewhere), exp via ex2.approx of
+// y log2 e, rcp / rsqrt .approx (1-2 ulp).  Every use is an O(1)-conditioned step of
+// a result checked to 1e-5 against the oracle; the f32 operating range (R13) keeps
+// the arguments normal.  The slow bin keeps the library functions (fm_log_wide).
 __device__ __forceinline__ float fm_log_wide(float a) { return logf(a); }
+// log whose absolute error is multiplied by a large factor (v log(x/(v+rho)) in the U
+// expansion, where v eta cancels towards its root): the accurate library logf in f32
+__device__ __forceinline__ float fm_log_acc(float a) { return logf(a); }
+#if B200_F32FAST
+__device__ __forceinline__ float fm_log(float a) { return __logf(a); }
+__device__ __forceinline__ float fm_exp(float y) { return __expf(fmaxf(y, -87.0f)); }
+__device__ __forceinline__ float fm_exp_nc(float y) { return __expf(y); }
+__device__ __forceinline__ float fm_rcp(float a) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
+    return r;
+}
+__device__ __forceinline__ float fm_div(float x, float y) { return x * fm_rcp(y); }
+__device__ __forceinline__ float fm_rsqrt(float a) {
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
+    return r;
+}
+#else
 __device__ __forceinline__ float fm_log(float a) { return logf(a); }
 __device__ __forceinline__ float fm_exp(float y) { return expf(y); }
 __device__ __forceinline__ float fm_exp_nc(float y) { return expf(y); }
 __device__ __forceinline__ float fm_rcp(float a) { return __frcp_rn(a); }
 __device__ __forceinline__ float fm_div(float x, float y) { return x / y; }
 __device__ __forceinline__ float fm_rsqrt(float a) { return rsqrtf(a); }
+#endif
 
 }  // namespace b200

@@ -155,6 +155,16 @@ def u_term_thresholds(kmin: int = 3, kmax: int = KMAX - 1, bits: int = 56):
     return out
 
 
+def f32_down_bits(c: float) -> int:
+    """Bits of the largest float32 <= c (c > 0)."""
+    import struct
+    import numpy as np
+    f = np.float32(c)
+    if float(f) > c:
+        f = np.nextafter(f, np.float32(0))
+    return struct.unpack("<I", struct.pack("<f", float(f)))[0]
+
+
 def hiword(c: float) -> int:
     import struct
     return struct.unpack("<Q", struct.pack("<d", c))[0] >> 32
@@ -216,6 +226,15 @@ def render() -> str:
     lines.append("// dispatch thresholds: IEEE high words (gen_tables.THRESHOLDS)")
     for k, c in THRESHOLDS.items():
         lines.append("#define B200_HW_%s 0x%08Xu   // %r" % (k, hiword(c), c))
+    lines.append("// f32 dispatch keys: float bit patterns (non-negative floats: bit order = value")
+    lines.append("// order).  \"a > C\" is bits(a) > bits(C_dn), C_dn = the largest float <= C")
+    lines.append("// (exact for float a); \"a >= rho_K\" is bits(a) >= bits(rho_K) (integers)")
+    for k, c in THRESHOLDS.items():
+        if k in ("LO", "HI"):
+            continue                      # the f64 range; f32 uses LO32 / HI32
+        lines.append("#define B200_F32_%s 0x%08Xu   // %r" % (k, f32_down_bits(c), c))
+    for K, r in u_term_thresholds().items():
+        lines.append("#define B200_F32_RHO_K%d 0x%08Xu   // %d" % (K, f32_down_bits(float(r)), r))
     lines.append("// rho from which K U-terms leave a first omitted term <= 2^-56 (R12):")
     lines.append("// B200_HW_RHO_K<K> = high word of that (integer) rho")
     for K, r in u_term_thresholds().items():

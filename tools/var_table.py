@@ -10,5 +10,6 @@ for k, v in d["sets"].items():
 print("grid".ljust(8) + "".join(f"{d['bench_grid_ms'][n].get('ivkv', float('nan')):9.3f}" for n in names))
 print("grid_iv".ljust(8) + "".join(f"{d['bench_grid_ms'][n]['log_iv']:9.3f}" for n in names))
 print("grid_kv".ljust(8) + "".join(f"{d['bench_grid_ms'][n]['log_kv']:9.3f}" for n in names))
+print("grid_f32".ljust(8) + "".join(f"{d['bench_grid_ms'][n].get('ivkv32', float('nan')):9.3f}" for n in names))
 md = max(v[n].get("ivkv", {}).get("maxdiff", 0) for v in d["sets"].values() for n in names)
 print("max output diff vs first variant:", md)

@@ -51,6 +51,9 @@ def run(names, n=20_000_000, reps=5):
         if hasattr(L, "b200_log_ivkv_f64"):
             L.b200_log_ivkv_f64.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_void_p]
             L.b200_log_ivkv_f64.restype = ctypes.c_int
+        if hasattr(L, "b200_log_ivkv_f32"):
+            L.b200_log_ivkv_f32.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_void_p]
+            L.b200_log_ivkv_f32.restype = ctypes.c_int
         libs[nm] = L
     g = torch.Generator(device=dev).manual_seed(0)
     sets = {}
@@ -106,10 +109,26 @@ def run(names, n=20_000_000, reps=5):
                 row["ivkv"] = {"ms": round(e0.elapsed_time(e1) / reps, 4),
                                "maxdiff": max(float(((o1 - ref["log_iv"]).abs() / ref["log_iv"].abs().clamp_min(1.0)).max()),
                                               float(((o2 - ref["log_kv"]).abs() / ref["log_kv"].abs().clamp_min(1.0)).max()))}
+            if hasattr(L, "b200_log_ivkv_f32"):
+                v32, x32 = v.float(), xx.float()
+                o1, o2 = torch.empty_like(v32), torch.empty_like(v32)
+                L.b200_log_ivkv_f32(v32.data_ptr(), x32.data_ptr(), o1.data_ptr(), o2.data_ptr(), n, s)
+                if "ref32" not in ref:
+                    ref["ref32"] = (o1.clone(), o2.clone())
+                md = max(float(((o1 - ref["ref32"][0]).abs() / ref["ref32"][0].abs().clamp_min(1.0)).max()),
+                         float(((o2 - ref["ref32"][1]).abs() / ref["ref32"][1].abs().clamp_min(1.0)).max()))
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(reps):
+                    L.b200_log_ivkv_f32(v32.data_ptr(), x32.data_ptr(), o1.data_ptr(), o2.data_ptr(), n, s)
+                e1.record()
+                torch.cuda.synchronize()
+                row["ivkv32"] = {"ms": round(e0.elapsed_time(e1) / reps, 4), "maxdiff": md}
+                del v32, x32, o1, o2
             res.setdefault(sname, {})[nm] = row
     # bench-grid totals (sum over the 11 order slices)
     tot = {nm: {fn: round(sum(res[f"v={2 ** j}"][nm][fn]["ms"] for j in range(11)), 3)
-                for fn in ("log_iv", "log_kv", "ivkv") if fn in res["v=1"][nm]} for nm in names}
+                for fn in ("log_iv", "log_kv", "ivkv", "ivkv32") if fn in res["v=1"][nm]} for nm in names}
     print(json.dumps({"sets": res, "bench_grid_ms": tot}, indent=1))
 
 
