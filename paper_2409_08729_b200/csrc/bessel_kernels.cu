@@ -287,8 +287,11 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 template <typename T, int FN>
 constexpr int smem_bytes() { return 4 * TILE * int(sizeof(T)) + TILE * 2; }   // stage[2][2][TILE] + idx[TILE]
 
+#ifndef B200_MINB32
+#define B200_MINB32 6        // CTAs per SM for the f32 kernels (40 registers; 4 and 5 measured slower)
+#endif
 template <typename T, int FN, bool TMA>
-__global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B200_MINB_IK : B200_MINB_K)
+__global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I ? B200_MINB : FN == FN_IK ? B200_MINB_IK : B200_MINB_K)
     bessel_eval_kernel(const T *__restrict__ vin, const T *__restrict__ xin, T *__restrict__ out,
                        T *__restrict__ out2, int64_t n) {
     constexpr int NOUT = FN == FN_IK ? 2 : 1;         // results per element (out, out2)
@@ -302,7 +305,7 @@ __global__ void __launch_bounds__(TPB, FN == FN_I ? B200_MINB : FN == FN_IK ? B2
     constexpr int VEC = 16 / int(sizeof(T));          // elements per 16 bytes (bulk-copy granule)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t ntiles = (n + TILE - 1) / TILE;
-    fm_tables_init();
+    fm_tables_init();   // the f64 log table (the f32 kernels use it in the double K recurrence)
     auto tile_rem = [&](int64_t t) { return int(n - t * TILE < TILE ? n - t * TILE : TILE); };
 
     // stage tile t into buffer (t / gridDim.x) & 1

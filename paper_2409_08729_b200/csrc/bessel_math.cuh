@@ -144,6 +144,9 @@ template <typename T, bool IS_K>
 __device__ __forceinline__ T mu_series(T v, T rx) {
     const T mu = T(4) * v * v;
     const T c = (IS_K ? T(0.125) : T(-0.125)) * rx;
+#if B200_MUF
+    const T z = c * mu;                          // factor = fma(c, -(2k-1)^2, c mu) / k
+#endif
     T term = T(1), s = T(1);
 #pragma unroll
     for (int k = 1; k <= KMU; k += 4) {        // four terms per stop test
@@ -151,7 +154,11 @@ __device__ __forceinline__ T mu_series(T v, T rx) {
         for (int u = 0; u < 4 && k + u <= KMU; ++u) {
             const int kk = k + u;
             const T inv_k = c_inv_k<T>(kk);
+#if B200_MUF
+            term *= fma(c, T(-(2 * kk - 1) * (2 * kk - 1)), z) * inv_k;
+#else
             term *= (mu - T((2 * kk - 1) * (2 * kk - 1))) * (c * inv_k);
+#endif
             s += term;
         }
         if (k >= 4 && fabs(term) <= Tr<T>::eps * T(0.25) * fabs(s)) break;

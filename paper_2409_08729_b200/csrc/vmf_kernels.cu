@@ -23,6 +23,10 @@ int set_err(int code, const char *msg);    // bessel_kernels.cu: per-thread last
 int cuda_err(cudaError_t e, const char *where);
 
 constexpr int CS_TPB = 256;
+#ifndef B200_CS_ROWS
+#define B200_CS_ROWS 8
+#endif
+constexpr int CS_ROWS = B200_CS_ROWS;       // rows in flight per thread in the column-sum stream
 
 template <typename T> struct VecOf;
 template <> struct VecOf<float> { using V = float4; static constexpr int N = 4; };
@@ -38,7 +42,7 @@ __device__ __forceinline__ void vadd(double *acc, const double2 &a) {
 // Stage 1: CTA (bx, by) sums rows [by*rows_per, (by+1)*rows_per) of the
 // column slab [bx*CW, bx*CW + CW).  Each thread owns VN consecutive columns
 // and streams its rows with VN-wide loads (a warp reads 32*VN*sizeof(T)
-// contiguous bytes per row); 4 rows in flight per thread.
+// contiguous bytes per row); CS_ROWS rows in flight per thread.
 template <typename T, bool VEC>
 __global__ void __launch_bounds__(CS_TPB) colsum_partial_kernel(const T *__restrict__ X, int64_t n, int64_t d,
                                                                 int64_t ld, int64_t rows_per,
@@ -57,13 +61,14 @@ __global__ void __launch_bounds__(CS_TPB) colsum_partial_kernel(const T *__restr
             using V = typename VecOf<T>::V;
             const T *p = X + r0 * ld + c0;
             int64_t r = r0;
-            for (; r + 4 <= r1; r += 4) {
-                V a0 = __ldcs(reinterpret_cast<const V *>(p));
-                V a1 = __ldcs(reinterpret_cast<const V *>(p + ld));
-                V a2 = __ldcs(reinterpret_cast<const V *>(p + 2 * ld));
-                V a3 = __ldcs(reinterpret_cast<const V *>(p + 3 * ld));
-                vadd(acc, a0); vadd(acc, a1); vadd(acc, a2); vadd(acc, a3);
-                p += 4 * ld;
+            // CS_ROWS rows in flight per thread (16-byte loads, streaming cache hint)
+            for (; r + CS_ROWS <= r1; r += CS_ROWS) {
+                V a[CS_ROWS];
+#pragma unroll
+                for (int q = 0; q < CS_ROWS; ++q) a[q] = __ldcs(reinterpret_cast<const V *>(p + q * ld));
+#pragma unroll
+                for (int q = 0; q < CS_ROWS; ++q) vadd(acc, a[q]);
+                p += CS_ROWS * ld;
             }
             for (; r < r1; ++r, p += ld) vadd(acc, __ldcs(reinterpret_cast<const V *>(p)));
         } else {
@@ -84,21 +89,33 @@ __global__ void __launch_bounds__(CS_TPB) colsum_partial_kernel(const T *__restr
 
 // Stage 2: colsum[j] (+)= sum_s part[s*d + j] in a fixed order: warp w of a
 // CTA sums slabs w, w + 8, w + 16, ... of 32 consecutive columns (one 256-byte
-// row segment per load), then the 8 warp partials are added in warp order --
-// deterministic for a given slab count, and d/32 CTAs instead of d/256 keep
-// enough loads in flight for the small-d case.
+// row segment per load) into four interleaved accumulators (four independent
+// loads in flight per warp instead of one dependent chain), combined in a fixed
+// order, then the 8 warp partials are added in warp order -- deterministic for a
+// given slab count.  d/32 CTAs.  Block 0 also writes the row-count slot
+// colsum[d] (+)= n when with_count (no separate launch).
 constexpr int CR_WARPS = 8;
 __global__ void __launch_bounds__(32 * CR_WARPS) colsum_reduce_kernel(const double *__restrict__ part, int64_t nslab,
                                                                      int64_t d, double *__restrict__ colsum,
-                                                                     int accumulate) {
+                                                                     int accumulate, int with_count, double n_rows) {
     __shared__ double sh[CR_WARPS][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (with_count && blockIdx.x == 0 && threadIdx.x == 0) colsum[d] = accumulate ? colsum[d] + n_rows : n_rows;
     for (int64_t c0 = int64_t(blockIdx.x) * 32; c0 < d; c0 += int64_t(gridDim.x) * 32) {
         const int64_t j = c0 + lane;
-        double s = 0.0;
-        if (j < d)
-            for (int64_t k = w; k < nslab; k += CR_WARPS) s += part[k * d + j];
-        sh[w][lane] = s;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        if (j < d) {
+            const double *p = part + j;
+            int64_t k = w;
+            for (; k + 3 * CR_WARPS < nslab; k += 4 * CR_WARPS) {
+                s0 += p[k * d];
+                s1 += p[(k + CR_WARPS) * d];
+                s2 += p[(k + 2 * CR_WARPS) * d];
+                s3 += p[(k + 3 * CR_WARPS) * d];
+            }
+            for (; k < nslab; k += CR_WARPS) s0 += p[k * d];
+        }
+        sh[w][lane] = (s0 + s1) + (s2 + s3);
         __syncthreads();
         if (w == 0 && j < d) {
             double t = sh[0][lane];
@@ -189,25 +206,41 @@ __global__ void __launch_bounds__(FIT_TPB) vmf_fit_kernel(const double *__restri
     // MLE: d logLik/dkappa = Rbar - A_p(kappa) (A_p strictly increasing), so
     // the maximiser is the root; safeguarded Newton from kappa2 with a
     // bracket [lo, hi] (lo: A < Rbar, hi: A > Rbar), bisection fallback.
+    // Stop rule: A_p is exp of a difference of two log I values, each carrying an
+    // absolute error ~ eps |log I| (R15), so near the root g = A_p - Rbar
+    // is noise of that size and Newton steps stop contracting instead of reaching
+    // 4e-16 k.  Stop when |g| is inside that error bound, when a step is below
+    // 4e-16 k or no longer at most half the previous one (quadratic convergence
+    // over), and return the evaluated point with the smallest |g| together with its
+    // A_p and log I (no re-evaluation).
     double lo = 0.0, hi = CUDART_INF;
     double k = (k2 > 0.0 && isfinite(k2)) ? k2 : k0;
     int it = 0;
+    double A = 0.0, lil = 0.0;
+    double kb = k, Ab = 0.0, lilb = 0.0, gb = CUDART_INF, prev = CUDART_INF;
     for (; it < 100; ++it) {
-        double lil;
-        const double A = a_p(p, k, s_l, lil);
+        A = a_p(p, k, s_l, lil);
         const double g = A - rbar;
-        if (g == 0.0) break;
+        if (fabs(g) < gb) { gb = fabs(g); kb = k; Ab = A; lilb = lil; }
+        // |g| within the error bound of A_p itself (64 eps max(|log I|, 1) relative, R15):
+        // k is the root to the precision the Bessel values allow
+        if (fabs(g) <= 64.0 * 1.1102230246251565e-16 * fmax(fabs(lil), 1.0) * A) { ++it; break; }
         if (g < 0.0) lo = k; else hi = k;
         const double dA = 1.0 - A * A - (p - 1.0) / k * A;
         double kn = k - g / dA;
-        if (!(kn > lo && kn < hi) || !isfinite(kn)) kn = isfinite(hi) ? 0.5 * (lo + hi) : 2.0 * k;
+        const bool newton = kn > lo && kn < hi && isfinite(kn);
+        if (!newton) kn = isfinite(hi) ? 0.5 * (lo + hi) : 2.0 * k;
         const double step = fabs(kn - k);
+        ++it;
+        if (step <= 4e-16 * k) break;
+        if (newton && step > 0.5 * prev) break;
+        if (isfinite(hi) && (hi - lo) <= 4e-16 * hi) break;
+        prev = newton ? step : CUDART_INF;
         k = kn;
-        if (step <= 4e-16 * k) { ++it; break; }
-        if (isfinite(hi) && (hi - lo) <= 4e-16 * hi) { ++it; break; }
     }
-    double lil;
-    const double A = a_p(p, k, s_l, lil);
+    k = kb;
+    A = Ab;
+    lil = lilb;
     if (w0) {
         stats[4] = k;
         stats[5] = (0.5 * p - 1.0) * log(k) - 0.5 * p * log(2.0 * CUDART_PI) - lil + k * rbar;
@@ -296,7 +329,7 @@ static int colsum_impl(const T *X, int64_t n, int64_t d, int64_t ld, double *col
     if (d == 0 && !with_count) return B200_OK;
     if (!X && n > 0) return set_err(B200_ERR_INVALID_ARGUMENT, "vmf_colsum: null X");
     if (!colsum) return set_err(B200_ERR_INVALID_ARGUMENT, "vmf_colsum: null colsum");
-    if (with_count) {
+    if (with_count && (d == 0 || n == 0)) {            // otherwise the reduce kernel writes the slot
         count_slot_kernel<<<1, 1, 0, s>>>(colsum + d, double(n), accumulate);
         g_launches.fetch_add(1, std::memory_order_relaxed);
         cudaError_t e = cudaGetLastError();
@@ -329,7 +362,8 @@ static int colsum_impl(const T *X, int64_t n, int64_t d, int64_t ld, double *col
     else
         colsum_partial_kernel<T, false><<<grid, CS_TPB, 0, s>>>(X, n, d, ld, rows_per, part);
     const int64_t rb = (d + 31) / 32;
-    colsum_reduce_kernel<<<unsigned(rb < 4096 ? rb : 4096), 32 * CR_WARPS, 0, s>>>(part, nslab, d, colsum, accumulate);
+    colsum_reduce_kernel<<<unsigned(rb < 4096 ? rb : 4096), 32 * CR_WARPS, 0, s>>>(part, nslab, d, colsum, accumulate,
+                                                                                 with_count, double(n));
     g_launches.fetch_add(2, std::memory_order_relaxed);
     return cuda_err(cudaGetLastError(), "vmf colsum launch");
 }

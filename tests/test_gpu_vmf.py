@@ -125,3 +125,41 @@ def test_full_size_features(B, d):
     assert abs(s[3] - k2) <= 1e-9 * k2 and abs(s[4] - km) <= 1e-9 * km
     del X
     torch.cuda.empty_cache()
+
+
+def test_colsum_concurrent_streams(B):
+    """Column sums of two different matrices enqueued back to back on two streams with no
+    synchronisation between them: each equals its single-stream result (the partials
+    scratch is per (device, stream); include/bessel_b200.h thread-safety contract)."""
+    Xa, _ = workloads.vmf_features(20_000, 2048, rbar=0.3, seed=5, device="cuda:0")
+    Xb, _ = workloads.vmf_features(20_000, 2048, rbar=0.6, seed=6, device="cuda:0")
+    ra = B.vmf_colsum(Xa).clone()
+    rb = B.vmf_colsum(Xb).clone()
+    torch.cuda.synchronize()
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    for _ in range(5):
+        with torch.cuda.stream(sa):
+            ga = B.vmf_colsum(Xa)
+        with torch.cuda.stream(sb):
+            gb = B.vmf_colsum(Xb)
+        with torch.cuda.stream(sa):
+            ga2 = B.vmf_colsum(Xa)
+        torch.cuda.synchronize()
+        assert torch.equal(ga, ra) and torch.equal(gb, rb) and torch.equal(ga2, ra)
+
+
+def test_with_count_layout_and_fit(B):
+    """with_count: d column sums followed by the row count in one buffer (the single
+    all-reduce of a sharded fit); vmf_fit_from_colsum(buf) reads n from the buffer and
+    equals the fit with an explicit n_total.  accumulate adds both parts."""
+    X, _ = workloads.vmf_features(3001, 256, rbar=0.4, seed=9, device="cuda:0", dtype=torch.float64)
+    buf = B.vmf_colsum(X, with_count=True)
+    assert buf.shape == (257,) and float(buf[256]) == 3001.0
+    assert torch.equal(buf[:256], B.vmf_colsum(X))
+    mu1, st1 = B.vmf_fit_from_colsum(buf)
+    mu2, st2 = B.vmf_fit_from_colsum(buf[:256].clone(), 3001)
+    assert torch.equal(mu1, mu2) and torch.equal(st1, st2)
+    two = B.vmf_colsum(X, out=buf.clone(), accumulate=True, with_count=True)
+    assert float(two[256]) == 6002.0 and torch.allclose(two[:256], 2 * buf[:256], rtol=1e-15, atol=0)
+    mu3, st3 = B.vmf_fit(X)
+    assert torch.equal(mu3, mu1) and torch.equal(st3, st1)
