@@ -123,6 +123,9 @@ constexpr int KMU = 26;
 #ifndef B200_MUF
 #define B200_MUF 1
 #endif
+#ifndef B200_MU2U
+#define B200_MU2U 0
+#endif
 
 // Wide-range guard: the fast paths form 1/x, v^2 + x^2 and 1/rho, which stay
 // normal for arguments below BIG; beyond it the same formulas run rescaled or
@@ -414,10 +417,13 @@ __device__ __forceinline__ void log_bessel_mu_ik(T v, T x, T &li, T &lk) {
     const T z = c * mu;
 #endif
     // terms in (odd, even) pairs, fully unrolled: (2k-1)^2 and 1/k are constants
+#ifndef B200_MU_STEP
+#define B200_MU_STEP 4
+#endif
 #pragma unroll
-    for (int k = 1; k < KMU; k += 4) {         // four terms per stop test (KMU = 4*6 + 2)
+    for (int k = 1; k < KMU; k += B200_MU_STEP) {   // B200_MU_STEP terms per stop test (KMU = 26)
 #pragma unroll
-        for (int u = 0; u < 4 && k + u <= KMU; u += 2) {
+        for (int u = 0; u < B200_MU_STEP && k + u <= KMU; u += 2) {
             const int k1 = k + u;
             const T i1 = c_inv_k<T>(k1), i2 = c_inv_k<T>(k1 + 1);
 #if B200_MUF
@@ -868,6 +874,11 @@ __device__ __forceinline__ int select_eval_hw(double v, double x, uint32_t hv, u
                  : m >= B200_HW_RHO(B200_KU_C) ? E_UC : E_U13;
     const int ef = hx > hw_split ? E_FB_B : E_FB_A;
     const int e = is_u_hw(hv, hx) ? eu : ef;
+#if B200_MU2U
+    // mu region with rho >= rho_10 (61): the U expansion with the R12 term count meets
+    // the same 2^-56 truncation bound for every t and costs less than the mu series
+    if (m >= B200_HW_RHO(B200_KU_C)) return is_mu_hw(v, x, hv, hx) ? eu : e;
+#endif
     return is_mu_hw(v, x, hv, hx) ? E_MU : e;
 }
 __device__ __forceinline__ int select_eval(double v, double x, uint32_t hw_split) {

@@ -85,7 +85,11 @@ __device__ __forceinline__ double fm_exp_core(double y) {
     p = fma(p, r, c_fm.exp_c3);
     p = fma(p, r, 0.5);
     p = fma(p, r * r, r);
+#if B200_SMEM_LOG && B200_SMEM_EXP
+    const double2 T = s_exptab[k & (B200_EXP_TAB_N - 1)];
+#else
     const double2 T = __ldg(&g_exptab[k & (B200_EXP_TAB_N - 1)]);
+#endif
     const double res = T.x + fma(T.x, p, T.y);
     return __hiloint2double(__double2hiint(res) + ((k >> 6) << 20), __double2loint(res));
 }
@@ -93,12 +97,21 @@ __device__ __forceinline__ double fm_exp_core(double y) {
 #ifndef B200_SMEM_LOG
 #define B200_SMEM_LOG 1
 #endif
+#ifndef B200_SMEM_EXP
+#define B200_SMEM_EXP 0
+#endif
 #if B200_SMEM_LOG
 // {1/c_i, -log(1/c_i)} in shared memory (filled by fm_tables_init at kernel start)
 static __shared__ double2 s_logtab[1 << B200_LOG_TAB_BITS];
+#if B200_SMEM_EXP
+static __shared__ double2 s_exptab[B200_EXP_TAB_N];
+#endif
 __device__ __forceinline__ void fm_tables_init() {
     for (int i = threadIdx.x; i < (1 << B200_LOG_TAB_BITS); i += blockDim.x)
         s_logtab[i] = make_double2(g_logtab[i].invc, g_logtab[i].thi);
+#if B200_SMEM_EXP
+    for (int i = threadIdx.x; i < B200_EXP_TAB_N; i += blockDim.x) s_exptab[i] = g_exptab[i];
+#endif
     __syncthreads();
 }
 #else
