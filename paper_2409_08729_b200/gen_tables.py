@@ -209,6 +209,11 @@ def render() -> str:
     lines.append("")
     lines.append("// 1/k, k = 0..400 (entry 0 unused)")
     lines.append("#define B200_INV_INIT { 0.0, %s }" % ", ".join("%.17e" % (1.0 / k) for k in range(1, 401)))
+    import math
+    from fractions import Fraction
+    lines.append("// 1/k! for k = 0..30 (correctly rounded)")
+    lines.append("#define B200_INVFACT_INIT { %s }" % ", ".join(
+        "%.17e" % float(Fraction(1, math.factorial(k))) for k in range(0, 31)))
     lines.append("")
     lines.append("// f64 log table (csrc/fastmath.cuh): {1/c_i, -log(1/c_i) hi, lo, 0}, i = 0..%d" % ((1 << LOG_TAB_BITS) - 1))
     lines.append("#define B200_LOG_TAB_BITS %d" % LOG_TAB_BITS)
