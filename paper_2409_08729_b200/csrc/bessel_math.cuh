@@ -135,7 +135,7 @@ constexpr int KMU = 26;
 #define B200_MU2U 0
 #endif
 #ifndef B200_MUFACT
-#define B200_MUFACT 1
+#define B200_MUFACT 2
 #endif
 
 // Wide-range guard: the fast paths form 1/x, v^2 + x^2 and 1/rho, which stay
@@ -428,6 +428,17 @@ __device__ __forceinline__ void log_bessel_mu_ik(T v, T x, T &li, T &lk) {
     const T c = T(0.125) * rx;
     const T z = c * (T(4) * v * v);
     T tk = T(1), si = T(1), sk = T(1);
+#if B200_MUFACT == 2
+    // even / odd partial sums: S_K = E + O, S_I = E - O (3 FP64 operations per term)
+    T ev = T(1), od = T(0);
+#define B200_MU_T(k)                                                          \
+    {                                                                         \
+        tk *= fma(c, T(-double((2 * (k) - 1) * (2 * (k) - 1))), z);          \
+        if ((k) & 1) od = fma(tk, c_invfact<T>(k), od);                       \
+        else ev = fma(tk, c_invfact<T>(k), ev);                               \
+    }
+#define B200_MU_STOP(k) if (fabs(tk) * c_invfact<T>(k) <= Tr<T>::eps * T(0.25) * fabs(ev - od)) goto mu_done;
+#else
 #define B200_MU_T(k)                                                          \
     {                                                                         \
         tk *= fma(c, T(-double((2 * (k) - 1) * (2 * (k) - 1))), z);          \
@@ -436,6 +447,7 @@ __device__ __forceinline__ void log_bessel_mu_ik(T v, T x, T &li, T &lk) {
         sk = fma(tk, f, sk);                                                  \
     }
 #define B200_MU_STOP(k) if (fabs(tk) * c_invfact<T>(k) <= Tr<T>::eps * T(0.25) * fabs(si)) goto mu_done;
+#endif
     B200_MU_T(1) B200_MU_T(2) B200_MU_T(3) B200_MU_T(4)
     B200_MU_T(5) B200_MU_T(6) B200_MU_T(7) B200_MU_T(8) B200_MU_STOP(8)
     B200_MU_T(9) B200_MU_T(10) B200_MU_T(11) B200_MU_T(12) B200_MU_STOP(12)
@@ -446,6 +458,10 @@ __device__ __forceinline__ void log_bessel_mu_ik(T v, T x, T &li, T &lk) {
 #undef B200_MU_T
 #undef B200_MU_STOP
 mu_done:
+#if B200_MUFACT == 2
+    si = ev - od;
+    sk = ev + od;
+#endif
     const T SI = fabs(si), SK = fabs(sk);
     li = x + T(0.5) * fm_log(SI * SI * rx * hc<T>(HC_INV2PI));
     lk = -x + T(0.5) * fm_log(SK * SK * rx * hc<T>(HC_PIO2));
@@ -736,25 +752,26 @@ __device__ __forceinline__ T trap_kmu(T mu, T x, T &rho) {
     const T Em = fm_exp(mu * h), Emi = fm_rcp(Em);
     const T eh = fm_exp(h);
     const T cm = Em + Emi, cp = fma(Em, eh, Emi * fm_rcp(eh));
-    T ap = T(2), ac = cm, bp = T(2), bc = cp;          // C_{k-1}, C_k (orders mu, mu+1), k = 1
-    T A = T(1), B = T(1), sp = T(0), sk = s1;
+    // (a0, a1) = (C_{k-1}, C_k) for order mu, (b0, b1) for mu+1, (x0, x1) = (s_{k-1}, s_k):
+    // each trip overwrites the older of every pair with the next value (no register
+    // moves in the loop), k = 1 at entry
+    T a0 = T(2), a1 = cm, b0 = T(2), b1 = cp;
+    T A = T(1), B = T(1), x0 = T(0), x1 = s1;
     const T m2x = T(-2) * x;
     for (int k = 1; k < 64; k += 2) {     // nodes k, k+1 per trip, stop test on the second
-        const T s2 = fma(c, sk, -sp);
-        const T e1 = fm_exp_nc(m2x * sk * sk), e2 = fm_exp_nc(m2x * s2 * s2);
-        const T an = fma(cm, ac, -ap), bn = fma(cp, bc, -bp);          // C_{k+1}
-        A = fma(e1, ac, A);
-        B = fma(e1, bc, B);
-        const T tb = e2 * bn;
-        A = fma(e2, an, A);
+        x0 = fma(c, x1, -x0);                                           // s_{k+1}
+        const T e1 = fm_exp_nc(m2x * x1 * x1), e2 = fm_exp_nc(m2x * x0 * x0);
+        a0 = fma(cm, a1, -a0);                                          // C_{k+1}
+        b0 = fma(cp, b1, -b0);
+        A = fma(e1, a1, A);
+        B = fma(e1, b1, B);
+        const T tb = e2 * b0;
+        A = fma(e2, a0, A);
         B += tb;
         if (tb <= B * Tr<T>::eps) break;
-        ap = an;                                                        // C_{k+1}
-        ac = fma(cm, an, -ac);                                          // C_{k+2}
-        bp = bn;
-        bc = fma(cp, bn, -bc);
-        sp = s2;
-        sk = fma(c, s2, -sk);
+        x1 = fma(c, x0, -x1);                                           // s_{k+2}
+        a1 = fma(cm, a0, -a1);                                          // C_{k+2}
+        b1 = fma(cp, b0, -b1);
     }
     rho = B * fm_rcp(A);
     return -x + fm_log(T(0.5) * h * A);
@@ -773,6 +790,7 @@ __device__ __forceinline__ T log_kv_fallback(T v, T x) {
         // x > 2, v <= 12.7: K_v / K_mu < 1e12, no rescaling needed.  The coefficient
         // 2 nu / x advances by one addition of 2/x per step (< 13 roundings)
         T km = T(1), kp = rho, a = mu * tox;
+#pragma unroll 2
         for (int i = 1; i < nl; ++i) {
             a += tox;
             const T kn = fma(a, kp, km);
@@ -789,6 +807,7 @@ __device__ __forceinline__ T log_kv_fallback(T v, T x) {
         // (double for both precisions)
         const double tx = double(T(2) * fm_rcp(x));
         double km = 1.0, kp = double(T(2) * S1 * fm_rcp(x * S)), a = double(mu) * tx;
+#pragma unroll 2
         for (int i = 1; i < nl; ++i) {
             a += tx;                                  // 2 (mu + i) / x
             const double kn = fma(a, kp, km);
@@ -850,6 +869,7 @@ __device__ __forceinline__ void log_ivkv_trap(T v, T x, T &ri, T &rk) {
     // kp = K_v / K_mu, kn = K_{v+1} / K_mu (one recurrence step past v); the
     // coefficient 2 nu / x advances by one addition of 2/x per step
     T km = T(1), kp = rho, a = mu * tox;
+#pragma unroll 2
     for (int i = 1; i <= nl; ++i) {
         a += tox;
         const T kn = fma(a, kp, km);
