@@ -46,9 +46,18 @@ namespace b200 {
 #define B200_ITEMS 6         // elements per thread per tile (tile = 1536 pairs)
 #endif
 constexpr int TPB = B200_TPB;
+#ifndef B200_ITEMS32
+#define B200_ITEMS32 7       // elements per thread per tile in the f32 kernels (6: +3.3% on the f32 grid)
+#endif
 constexpr int ITEMS = B200_ITEMS;
 constexpr int TILE = TPB * ITEMS;       // 1536 pairs per tile
 static_assert(TILE <= 4096, "s_idx packs a 12-bit tile index with the bin");
+// per-precision tile (f32 stages are half the bytes)
+template <typename T> struct TileOf {
+    static constexpr int items = sizeof(T) == 4 ? B200_ITEMS32 : B200_ITEMS;
+    static constexpr int tile = TPB * items;
+    static_assert(items <= 7 && tile <= 4096, "8-bit warp counters, 12-bit tile index");
+};
 constexpr int BIN_SLOW = 7;           // out-of-range / special inputs (slow_eval)
 #ifndef B200_WS
 #define B200_WS 0                     // 1: aligned operands take the pipelined kernel (bessel_ws_kernel)
@@ -144,10 +153,10 @@ __device__ __forceinline__ T eval_bin(int bin, T v, T x) {
     if (FN == FN_I) {
         switch (bin) {
             case E_MU: return log_bessel_mu<T, false, false>(v, x);
-            case E_UA: return log_bessel_u<T, false, KU_A, false>(v, x);
-            case E_UB: return log_bessel_u<T, false, KU_B, false>(v, x);
-            case E_UC: return log_bessel_u<T, false, KU_C, false>(v, x);
-            case E_U13: return log_bessel_u<T, false, 13, false>(v, x);
+            case E_UA: return log_bessel_u<T, false, KUs<T>::A, false>(v, x);
+            case E_UB: return log_bessel_u<T, false, KUs<T>::B, false>(v, x);
+            case E_UC: return log_bessel_u<T, false, KUs<T>::C, false>(v, x);
+            case E_U13: return log_bessel_u<T, false, KUs<T>::D, false>(v, x);
             case E_FB_A:
             case E_FB_B: return log_iv_series<T, false>(v, x);
             default: return slow_eval<T, FN>(v, x);
@@ -156,10 +165,10 @@ __device__ __forceinline__ T eval_bin(int bin, T v, T x) {
     const T av = fabs(v);
     switch (bin) {
         case E_MU: return log_bessel_mu<T, true, false>(av, x);
-        case E_UA: return log_bessel_u<T, true, KU_A, false>(av, x);
-        case E_UB: return log_bessel_u<T, true, KU_B, false>(av, x);
-        case E_UC: return log_bessel_u<T, true, KU_C, false>(av, x);
-        case E_U13: return log_bessel_u<T, true, 13, false>(av, x);
+        case E_UA: return log_bessel_u<T, true, KUs<T>::A, false>(av, x);
+        case E_UB: return log_bessel_u<T, true, KUs<T>::B, false>(av, x);
+        case E_UC: return log_bessel_u<T, true, KUs<T>::C, false>(av, x);
+        case E_U13: return log_bessel_u<T, true, KUs<T>::D, false>(av, x);
         case E_FB_A:
         case E_FB_B: return FN == FN_K_PAPER ? log_kv_integral_paper<T>(av, x) : log_kv_fallback<T, false>(av, x);
         default: return slow_eval<T, FN>(v, x);
@@ -175,17 +184,17 @@ __device__ __forceinline__ void eval_bin_ik(int bin, T v, T x, T &ri, T &rk) {
 #if B200_IFCHAIN
     // the cheap bins by compare-and-branch (warp-uniform after the sort); no jump table
     if (bin == E_MU) { log_bessel_mu_ik<T>(v, x, ri, rk); return; }
-    if (bin == E_UA) { log_bessel_u_ik<T, KU_A>(v, x, ri, rk); return; }
-    if (bin == E_UB) { log_bessel_u_ik<T, KU_B>(v, x, ri, rk); return; }
-    if (bin == E_UC) { log_bessel_u_ik<T, KU_C>(v, x, ri, rk); return; }
-    if (bin == E_U13) { log_bessel_u_ik<T, 13>(v, x, ri, rk); return; }
+    if (bin == E_UA) { log_bessel_u_ik<T, KUs<T>::A>(v, x, ri, rk); return; }
+    if (bin == E_UB) { log_bessel_u_ik<T, KUs<T>::B>(v, x, ri, rk); return; }
+    if (bin == E_UC) { log_bessel_u_ik<T, KUs<T>::C>(v, x, ri, rk); return; }
+    if (bin == E_U13) { log_bessel_u_ik<T, KUs<T>::D>(v, x, ri, rk); return; }
 #endif
     switch (bin) {
         case E_MU: log_bessel_mu_ik<T>(v, x, ri, rk); break;
-        case E_UA: log_bessel_u_ik<T, KU_A>(v, x, ri, rk); break;
-        case E_UB: log_bessel_u_ik<T, KU_B>(v, x, ri, rk); break;
-        case E_UC: log_bessel_u_ik<T, KU_C>(v, x, ri, rk); break;
-        case E_U13: log_bessel_u_ik<T, 13>(v, x, ri, rk); break;
+        case E_UA: log_bessel_u_ik<T, KUs<T>::A>(v, x, ri, rk); break;
+        case E_UB: log_bessel_u_ik<T, KUs<T>::B>(v, x, ri, rk); break;
+        case E_UC: log_bessel_u_ik<T, KUs<T>::C>(v, x, ri, rk); break;
+        case E_U13: log_bessel_u_ik<T, KUs<T>::D>(v, x, ri, rk); break;
         case E_FB_B:   // 2 < x <= 30
 #ifndef B200_IK_SERIES   // experiment switch: the power series for I on this band too
             log_ivkv_trap<T>(v, x, ri, rk);   // I from the K values (Wronskian + Miller ratio)
@@ -285,7 +294,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 //   4. (one thread) bulk store of the stage's result arrays to HBM; the
 //      buffer is reloaded only after the store has read it.
 template <typename T, int FN>
-constexpr int smem_bytes() { return 4 * TILE * int(sizeof(T)) + TILE * 2; }   // stage[2][2][TILE] + idx[TILE]
+constexpr int smem_bytes() { return 4 * TileOf<T>::tile * int(sizeof(T)) + TileOf<T>::tile * 2; }   // stage[2][2][TILE] + idx[TILE]
 
 #ifndef B200_MINB32
 #define B200_MINB32 6        // CTAs per SM for the f32 kernels (40 registers; 4 and 5 measured slower)
@@ -295,6 +304,7 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
     bessel_eval_kernel(const T *__restrict__ vin, const T *__restrict__ xin, T *__restrict__ out,
                        T *__restrict__ out2, int64_t n) {
     constexpr int NOUT = FN == FN_IK ? 2 : 1;         // results per element (out, out2)
+    constexpr int ITEMS = TileOf<T>::items, TILE = TileOf<T>::tile;   // shadow the f64 defaults
     // dynamic shared memory (smem_bytes<T, FN>()): stage[2][2][TILE], idx[TILE]
     extern __shared__ __align__(128) unsigned char s_dyn[];
     auto s_stage = reinterpret_cast<T (*)[2][TILE]>(s_dyn);                       // [buffer][v|x][element]
@@ -832,7 +842,7 @@ static int launch_eval(const T *v, const T *x, T *out, int64_t n, cudaStream_t s
     }
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
-    const int64_t ntiles = (n + TILE - 1) / TILE;
+    const int64_t ntiles = (n + TileOf<T>::tile - 1) / TileOf<T>::tile;
     const int64_t resident = int64_t(sms) * o;
     const int grid = int(ntiles < resident ? ntiles : resident);
     if (tma)

@@ -43,8 +43,12 @@ template <> struct Tr<float> {
 enum : int { HC_INV2PI = 0, HC_PIO2, HC_LNPI, HC_ETA_HI, HC_ETA_BAND, HC_PI2, HC_N };
 static __constant__ double c_hot_d[HC_N] = {0.5 / CUDART_PI, CUDART_PI / 2.0, 1.1447298858494002,
                                             B200_ETA_Z0_HI, 0.03, CUDART_PI * CUDART_PI};
+// f32: the eta band is |z - z0| < 0.12 (f64: 0.03): outside it rho + v log(x/(v+rho)) cancels
+// up to ~6x at 0.12 against ~17x at 0.04, and float rounding times that cancellation came
+// within 5% of the 1e-5 bar; the 8-term Taylor series of eta (radius |z0 - i| ~ 1.2) is
+// accurate to < 1e-8 on the wider band (profiles/r62/acc32.txt)
 static __constant__ float c_hot_f[HC_N] = {float(0.5 / CUDART_PI), float(CUDART_PI / 2.0), 1.1447298858494002f,
-                                           B200_ETA_Z0_HI_F, 0.03f, float(CUDART_PI * CUDART_PI)};
+                                           B200_ETA_Z0_HI_F, 0.12f, float(CUDART_PI * CUDART_PI)};
 template <typename T>
 __device__ __forceinline__ T hc(int i) {
     if constexpr (sizeof(T) == 8) return c_hot_d[i]; else return c_hot_f[i];
@@ -251,6 +255,13 @@ __device__ __forceinline__ T l1p_step(T p, T d) {
     else return l1p_step<T, NP, K - 1>(fma(p, d, T(l1p_coef<K, (NP <= 5)>())), d);
 }
 #endif
+// f32: first omitted U term <= 2^-28 (R17) -> log1p degree N with |d|^(N+1)/(N+1) <= 2^-28:
+// |d| < 4.6e-4 (K = 2, rho >= 270), 1.7e-3 (K = 3, rho >= 75), 5.3e-3 (K = 5, rho >= 24),
+// 0.011 (K = 9, rho >= 12)
+template <int KU> struct Log1pDeg32 { static constexpr int v = KU >= 9 ? 4 : KU >= 5 ? 3 : 2; };
+template <typename T, int KU> struct L1PDeg { static constexpr int v = Log1pDeg<KU>::v; };
+template <int KU> struct L1PDeg<float, KU> { static constexpr int v = Log1pDeg32<KU>::v; };
+
 template <typename T, int NP>
 __device__ __forceinline__ T log1p_small(T d) {
 #if B200_IMM
@@ -379,7 +390,7 @@ __device__ __forceinline__ T log_bessel_u(T v, T x) {
     const T veta = v_times_eta<T, SAFE>(v, x, vs, xs, rhos, rho);
     // log S + 1/2 log(y_true c) with y_true = s y
     const T c = IS_K ? hc<T>(HC_PIO2) : hc<T>(HC_INV2PI);
-    const T tail = log1p_small<T, Log1pDeg<KU>::v>(d) + T(0.5) * (fm_log(y * c) + ls);
+    const T tail = log1p_small<T, L1PDeg<T, KU>::v>(d) + T(0.5) * (fm_log(y * c) + ls);
     return IS_K ? tail - veta : veta + tail;
 }
 
@@ -411,8 +422,8 @@ __device__ __forceinline__ void log_bessel_u_ik(T v, T x, T &li, T &lk) {
     // log S_I = log1p(e + o), log S_K = log1p(e - o); one log of y for both:
     // 1/2 log(y pi/2) = 1/2 log(y/(2 pi)) + log(pi)
     const T hl = T(0.5) * fm_log(y * hc<T>(HC_INV2PI));
-    li = veta + (hl + log1p_small<T, Log1pDeg<KU>::v>(e + o));
-    lk = (hl + hc<T>(HC_LNPI)) + log1p_small<T, Log1pDeg<KU>::v>(e - o) - veta;
+    li = veta + (hl + log1p_small<T, L1PDeg<T, KU>::v>(e + o));
+    lk = (hl + hc<T>(HC_LNPI)) + log1p_small<T, L1PDeg<T, KU>::v>(e - o) - veta;
 }
 
 
@@ -742,7 +753,9 @@ __device__ __forceinline__ T temme_kmu(T mu, T x, T &sum, T &sum1) {
 // Returns log K_mu and rho = K_{mu+1} / K_mu.  12-17 nodes on the band.
 template <typename T>
 __device__ __forceinline__ T trap_kmu(T mu, T x, T &rho) {
-    const T h = hc<T>(HC_PI2) * fm_rcp(fma(T(0.8), x, T(42)));
+    // f64: h = pi^2 / (42 + 0.8 x) (measured largest admissible step for 2^-53, R14);
+    // f32: the error ~ exp(-pi^2 / h) only has to reach ~2^-26: h = pi^2 / (24 + 0.45 x)
+    const T h = hc<T>(HC_PI2) * fm_rcp(sizeof(T) == 8 ? fma(T(0.8), x, T(42)) : fma(T(0.45), x, T(24)));
     const T a = T(0.5) * h, a2 = a * a;
     // sinh(a) and 2 cosh(a) by their Taylor series (a <= 0.12: 5 terms exact to 2^-60)
     const T s1 = a * fma(a2 * T(1.0 / 6), fma(a2 * T(1.0 / 20), fma(a2 * T(1.0 / 42), fma(a2, T(1.0 / 72), T(1)), T(1)), T(1)), T(1));
@@ -952,6 +965,10 @@ __device__ __forceinline__ T log_kv_integral_paper(T v, T x) {
 #define B200_CAT(a, b) B200_CAT_(a, b)
 #define B200_HW_RHO(K) B200_CAT(B200_HW_RHO_K, K)
 constexpr int KU_A = B200_KU_A, KU_B = B200_KU_B, KU_C = B200_KU_C;
+// U term count per bin and precision: f64 by the 2^-56 bound (R12), f32 by 2^-28 (R17)
+template <typename T> struct KUs;
+template <> struct KUs<double> { static constexpr int A = KU_A, B = KU_B, C = KU_C, D = 13; };
+template <> struct KUs<float> { static constexpr int A = 2, B = 3, C = 5, D = 9; };
 static_assert(KU_A < KU_B && KU_B < KU_C && KU_C < 13, "U bins: increasing term counts below 13");
 enum : int { E_MU = 0, E_UA = 1, E_UB = 2, E_UC = 3, E_U13 = 4, E_FB_A = 5, E_FB_B = 6 };
 
@@ -984,8 +1001,9 @@ __device__ __forceinline__ bool mu_edge_f32(float v, float x) {
 }
 __device__ __forceinline__ int select_eval_f32(float v, float x, uint32_t hv, uint32_t hx, uint32_t split) {
     const uint32_t m = hv > hx ? hv : hx;
-    const int eu = m >= B200_CAT(B200_F32_RHO_K, B200_KU_A) ? E_UA : m >= B200_CAT(B200_F32_RHO_K, B200_KU_B) ? E_UB
-                 : m >= B200_CAT(B200_F32_RHO_K, B200_KU_C) ? E_UC : E_U13;
+    // f32 U bins: K = 2 / 3 / 5 / 9 (KUs<float>) from their 2^-28 thresholds (R17)
+    const int eu = m >= B200_F32U_RHO_K2 ? E_UA : m >= B200_F32U_RHO_K3 ? E_UB
+                 : m >= B200_F32U_RHO_K5 ? E_UC : E_U13;
     const int ef = hx > split ? E_FB_B : E_FB_A;
     const bool u = (hx > B200_F32_X19 && hv > B200_F32_V07) || hv > B200_F32_V12;
     bool mu = hx > B200_F32_X30 && hv <= B200_F32_V15;                   // x > 30 && v < 15.3919

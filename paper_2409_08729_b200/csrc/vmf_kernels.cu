@@ -27,6 +27,9 @@ constexpr int CS_TPB = 256;
 #define B200_CS_ROWS 8
 #endif
 constexpr int CS_ROWS = B200_CS_ROWS;       // rows in flight per thread in the column-sum stream
+#ifndef B200_CS_CTAS
+#define B200_CS_CTAS 8                      // column-sum CTAs per SM (row slabs x column slabs)
+#endif
 
 template <typename T> struct VecOf;
 template <> struct VecOf<float> { using V = float4; static constexpr int N = 4; };
@@ -347,7 +350,7 @@ static int colsum_impl(const T *X, int64_t n, int64_t d, int64_t ld, double *col
     const int CW = CS_TPB * (vec ? VN : 1);
     const int64_t ncol = (d + CW - 1) / CW;
     // ~8 CTAs per SM in total; each CTA streams a slab of rows
-    int64_t nslab = (8 * int64_t(sms_count(dev)) + ncol - 1) / ncol;
+    int64_t nslab = (B200_CS_CTAS * int64_t(sms_count(dev)) + ncol - 1) / ncol;
     if (nslab > n) nslab = n;
     if (nslab < 1) nslab = 1;
     const int64_t rows_per = (n + nslab - 1) / nslab;

@@ -240,6 +240,10 @@ def render() -> str:
         lines.append("#define B200_F32_%s 0x%08Xu   // %r" % (k, f32_down_bits(c), c))
     for K, r in u_term_thresholds().items():
         lines.append("#define B200_F32_RHO_K%d 0x%08Xu   // %d" % (K, f32_down_bits(float(r)), r))
+    lines.append("// f32 U bins: rho from which K terms leave a first omitted term <= 2^-28 (R17),")
+    lines.append("// float bits; the f32 kernels use K = 2 / 3 / 5 / 9")
+    for K, r in u_term_thresholds(kmin=1, kmax=12, bits=28).items():
+        lines.append("#define B200_F32U_RHO_K%d 0x%08Xu   // %d" % (K, f32_down_bits(float(r)), r))
     lines.append("// rho from which K U-terms leave a first omitted term <= 2^-56 (R12):")
     lines.append("// B200_HW_RHO_K<K> = high word of that (integer) rho")
     for K, r in u_term_thresholds().items():

@@ -19,24 +19,27 @@ SETS = {
 }
 
 
-def main(n=20000, seed=0):
+def main(n=20000, seed=0, dtype=torch.float64):
     rng = np.random.default_rng(seed)
     res = {}
     for name, ((v0, v1), (x0, x1)) in SETS.items():
         v = rng.uniform(v0, v1, n)
         x = np.exp(rng.uniform(np.log(x0), np.log(x1), n)) if x1 / x0 > 50 else rng.uniform(x0, x1, n)
-        vt = torch.tensor(v, device="cuda:0")
-        xt = torch.tensor(x, device="cuda:0")
+        if dtype == torch.float32:          # the oracle at the inputs the f32 kernels see
+            v = v.astype(np.float32).astype(np.float64)
+            x = x.astype(np.float32).astype(np.float64)
+        vt = torch.tensor(v, device="cuda:0", dtype=dtype)
+        xt = torch.tensor(x, device="cuda:0", dtype=dtype)
         row = {}
         for fn in ("iv", "kv"):
-            got = (B.log_iv if fn == "iv" else B.log_kv)(vt, xt).cpu().numpy()
+            got = (B.log_iv if fn == "iv" else B.log_kv)(vt, xt).double().cpu().numpy()
             ref = (oracle.log_iv if fn == "iv" else oracle.log_kv)(v, x)
             e = oracle.rel_err(got, ref)
             i = int(np.argmax(e))
             row[fn] = {"max": float(e[i]), "p99": float(np.quantile(e, 0.99)), "at": [float(v[i]), float(x[i])]}
         fi, fk = B.log_ivkv(vt, xt)
         for nm, got, ref in (("ivkv_i", fi, oracle.log_iv(v, x)), ("ivkv_k", fk, oracle.log_kv(v, x))):
-            e = oracle.rel_err(got.cpu().numpy(), ref)
+            e = oracle.rel_err(got.double().cpu().numpy(), ref)
             i = int(np.argmax(e))
             row[nm] = {"max": float(e[i]), "p99": float(np.quantile(e, 0.99)), "at": [float(v[i]), float(x[i])]}
         res[name] = row
@@ -47,7 +50,8 @@ def main(n=20000, seed=0):
 
 
 if __name__ == "__main__":
-    # usage: python tools/accuracy_report.py [out.json] [points per set]
-    r = main(int(sys.argv[2])) if len(sys.argv) > 2 else main()
+    # usage: python tools/accuracy_report.py [out.json] [points per set] [f32]
+    dt = torch.float32 if "f32" in sys.argv[3:] else torch.float64
+    r = main(int(sys.argv[2]), dtype=dt) if len(sys.argv) > 2 else main()
     if len(sys.argv) > 1:
         json.dump(r, open(sys.argv[1], "w"), indent=1)
