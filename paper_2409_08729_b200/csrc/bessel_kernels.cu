@@ -202,14 +202,13 @@ __device__ __forceinline__ void eval_bin_ik(int bin, T v, T x, T &ri, T &rk) {
 #endif
         case E_FB_A:   // x <= 2
 #ifndef B200_IK_SERIES_A
-            if constexpr (sizeof(T) == 8) {
-                // v < 1/2 keeps the power series: there |log I| can be << 1 (log I_0(x) ~ x^2/4)
-                // and log I = -log K_mu - log(...) would cancel to an absolute, not relative,
-                // error (R1)
-                if (x >= T(1e-6) && x <= T(2) && v >= T(0.5)) {
-                    log_ivkv_trap<T, true>(v, x, ri, rk);   // Temme K values, Wronskian + Miller ratio
-                    break;
-                }
+            // v < 1/2 keeps the power series: there |log I| can be << 1 (log I_0(x) ~ x^2/4)
+            // and log I = -log K_mu - log(...) would cancel to an absolute, not relative,
+            // error (R1).  f32: from x = 0.1, where the Miller values stay below
+            // ~(2 (v + M) / x)^M < 2e18 and K_{v+1} / K_mu < 1e27 (FLT_MAX 3.4e38)
+            if (x >= T(sizeof(T) == 8 ? 1e-6 : 0.1) && x <= T(2) && v >= T(0.5)) {
+                log_ivkv_trap<T, true>(v, x, ri, rk);   // Temme K values, Wronskian + Miller ratio
+                break;
             }
 #endif
             ri = log_iv_series<T, false>(v, x);

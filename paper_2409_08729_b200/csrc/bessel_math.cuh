@@ -906,7 +906,12 @@ __device__ __forceinline__ void log_ivkv_trap(T v, T x, T &ri, T &rk) {
     }
     // r = y1 / y0;  1 / (I_v K_mu) = x (K_{v+1} + r K_v) / K_mu
     rk = nl == 0 ? lk : lk + fm_log(km);
-    ri = -lk - fm_log(x * fma(km, y1, kp * y0) * fm_rcp(y0));
+    if constexpr (sizeof(T) == 8) {
+        ri = -lk - fm_log(x * fma(km, y1, kp * y0) * fm_rcp(y0));
+    } else {
+        // f32: kp y0 can pass FLT_MAX near x = 0.1 (~1e27 * 1e17); take the ratio first
+        ri = -lk - fm_log(x * fma(km, y1 * fm_rcp(y0), kp));
+    }
 }
 
 // ---------------------------------------------------------------- paper K

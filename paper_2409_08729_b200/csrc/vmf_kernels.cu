@@ -30,6 +30,9 @@ constexpr int CS_ROWS = B200_CS_ROWS;       // rows in flight per thread in the 
 #ifndef B200_CS_CTAS
 #define B200_CS_CTAS 8                      // column-sum CTAs per SM (row slabs x column slabs)
 #endif
+#ifndef B200_CS_CTAS_SMALL
+#define B200_CS_CTAS_SMALL 3                // the same when d spans at most two column slabs (2/3/4 measured)
+#endif
 
 template <typename T> struct VecOf;
 template <> struct VecOf<float> { using V = float4; static constexpr int N = 4; };
@@ -350,7 +353,10 @@ static int colsum_impl(const T *X, int64_t n, int64_t d, int64_t ld, double *col
     const int CW = CS_TPB * (vec ? VN : 1);
     const int64_t ncol = (d + CW - 1) / CW;
     // ~8 CTAs per SM in total; each CTA streams a slab of rows
-    int64_t nslab = (B200_CS_CTAS * int64_t(sms_count(dev)) + ncol - 1) / ncol;
+    // few column slabs (d <= 2 CW): fewer row slabs -- the partials (nslab x d doubles) and
+    // their reduce shrink, while 8 rows in flight per thread keep the stream fed
+    const int ctas = ncol <= 2 ? B200_CS_CTAS_SMALL : B200_CS_CTAS;
+    int64_t nslab = (ctas * int64_t(sms_count(dev)) + ncol - 1) / ncol;
     if (nslab > n) nslab = n;
     if (nslab < 1) nslab = 1;
     const int64_t rows_per = (n + nslab - 1) / nslab;

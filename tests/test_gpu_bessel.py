@@ -621,3 +621,23 @@ def test_pure_relative_accuracy_where_log_iv_is_small(B):
         i = int(np.argmax(e))
         assert e[i] <= TOL64, f"{name}: pure rel err {e[i]:.3e} at v={v[nz][i]!r} x={x[nz][i]!r}"
     assert np.all(np.abs(gi[~nz]) <= 1e-300)
+
+
+def test_fused_f32_temme_band(B):
+    """f32 fused pass on 0.1 <= x <= 2, 1/2 <= v <= 12.7, where log I comes from Temme's K values
+    by the Wronskian and Miller's ratio (float range: the ratio is formed before the product
+    with K_{v+1}/K_mu, which alone reaches ~1e27 at x = 0.1); edges of the band included."""
+    rng = np.random.default_rng(63)
+    v = rng.uniform(0.5, 12.69, 20_000)
+    x = workloads.log_uniform(20_000, 0.05, 2.0, seed=64)
+    v[:8] = [12.69, 12.69, 0.5, 0.5, 7.3, 12.69, 0.5, 3.0]
+    x[:8] = [0.1, 0.0999, 0.1, 2.0, 0.1000001, 2.0, 0.0999, 1.0]
+    v = v.astype(np.float32).astype(np.float64)
+    x = x.astype(np.float32).astype(np.float64)
+    gi, gk = _run_ivkv(B, v, x, torch.float32)
+    assert np.all(np.isfinite(gi)) and np.all(np.isfinite(gk))
+    ri, rk = oracle.log_iv(v, x), oracle.log_kv(v, x)
+    for name, got, ref in (("I", gi, ri), ("K", gk, rk)):
+        e = oracle.rel_err(got, ref)
+        i = int(np.argmax(e))
+        assert e[i] <= TOL32, f"fused f32 {name}: {e[i]:.3e} at v={v[i]!r} x={x[i]!r}"
