@@ -292,8 +292,13 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 //      (v, x) slots (each element is read and written by one thread only);
 //   4. (one thread) bulk store of the stage's result arrays to HBM; the
 //      buffer is reloaded only after the store has read it.
+#ifndef B200_PAD
+#define B200_PAD 1           // 1: f64 fused pass: sort keys costliest first, bins padded to 32-slot chunks
+#endif
+// slots of the sorted order: TILE, plus up to 7 * 31 padding slots (B200_PAD)
+template <typename T> constexpr int idx_slots() { return TileOf<T>::tile + (B200_PAD && sizeof(T) == 8 ? 256 : 0); }
 template <typename T, int FN>
-constexpr int smem_bytes() { return 4 * TileOf<T>::tile * int(sizeof(T)) + TileOf<T>::tile * 2; }   // stage[2][2][TILE] + idx[TILE]
+constexpr int smem_bytes() { return 4 * TileOf<T>::tile * int(sizeof(T)) + idx_slots<T>() * 2; }   // stage[2][2][TILE] + idx
 
 #ifndef B200_MINB32
 #define B200_MINB32 6        // CTAs per SM for the f32 kernels (40 registers; 4 and 5 measured slower)
@@ -304,6 +309,10 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
                        T *__restrict__ out2, int64_t n) {
     constexpr int NOUT = FN == FN_IK ? 2 : 1;         // results per element (out, out2)
     constexpr int ITEMS = TileOf<T>::items, TILE = TileOf<T>::tile;   // shadow the f64 defaults
+    // padded, costliest-first sort order with snake chunk dealing: the f64 fused pass only
+    // (measured: it gains on tiles mixing the fallback with cheap bins; the f32 and
+    // single-function kernels, whose fallback is cheap, lose 2-3% to the extra work)
+    constexpr bool PADK = B200_PAD && sizeof(T) == 8 && FN == FN_IK;
     // dynamic shared memory (smem_bytes<T, FN>()): stage[2][2][TILE], idx[TILE]
     extern __shared__ __align__(128) unsigned char s_dyn[];
     auto s_stage = reinterpret_cast<T (*)[2][TILE]>(s_dyn);                       // [buffer][v|x][element]
@@ -382,6 +391,7 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
         }
         int lb[ITEMS];
 #if B200_C32
+        static_assert(!PADK, "B200_C32 counts bins, B200_PAD sort keys");
         // packed 8-bit counters, incremented with 32-bit operations (a variable
         // 64-bit shift costs ~4 more instructions per element)
         uint32_t clo = 0, chi = 0;
@@ -405,7 +415,7 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
             lb[i] = -1;
             if (j < rem) {
                 lb[i] = bin_of<T, FN>(sv[j], sx[j]);
-                c8 += 1ull << (8 * lb[i]);
+                c8 += 1ull << (PADK ? 56 - 8 * lb[i] : 8 * lb[i]);   // PADK: sort key 7 - bin, costliest first
             }
         }
 #endif
@@ -419,7 +429,8 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
         if (lane == 31) s_wtot[warp] = incl;
         __syncthreads();
         uint64_t plo = 0, phi = 0;
-        int homo = 0;                // tile-homogeneous: 1 + its bin (CTA-uniform)
+        int homo = 0;                // tile-homogeneous: 1 + its sort key (CTA-uniform)
+        int nchunk = 0;              // B200_PAD: 32-slot chunks of the padded sorted order
         {
             // lanes 0..NW-1 of every warp scan the per-warp totals (16-bit fields);
             // the warp keeps the exclusive prefix of its own index
@@ -445,9 +456,31 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
                 if (ml | mh) homo = 1 + (ml ? (__ffsll(ml) - 16) >> 4 : 4 + ((__ffsll(mh) - 16) >> 4));
             }
 #endif
-            const uint64_t tp = tlo * ONES;
-            const uint64_t blo = tp - tlo;                                         // bases of bins 0..3
-            const uint64_t bhi = thi * ONES - thi + (tp >> 48) * ONES;             // bases of bins 4..7
+            // PADK: key k = 7 - bin (the costliest bins first), and in a mixed tile each
+            // key's run of slots starts on a 32-slot chunk boundary (sizes rounded up to
+            // multiples of 32: fields < 2^15, no carries), so no warp evaluates two methods
+            // in one chunk (a chunk mixing the fallback with a cheap bin runs the fallback's
+            // ~1000 instructions beside the other method); the padding slots hold 0xFFFF.
+            constexpr uint64_t F32 = 0xFFE0FFE0FFE0FFE0ull;
+            uint64_t blo, bhi;
+            if constexpr (PADK) {
+                // (a homogeneous tile computes the padded bases too and does not use them)
+                const uint64_t qlo = (tlo + 31 * ONES) & F32, qhi = (thi + 31 * ONES) & F32;
+                const uint64_t tp = qlo * ONES;
+                blo = tp - qlo;                                                    // padded bases of keys 0..3
+                bhi = qhi * ONES - qhi + (tp >> 48) * ONES;                        // padded bases of keys 4..7
+                nchunk = int(((bhi + qhi) >> 48) >> 5);                            // chunks of the padded order
+                // warp w fills the padding after key w: slots [base + count, base + round32(count))
+                const int sh = 16 * (warp & 3);
+                const int kb = int(((warp < 4 ? blo : bhi) >> sh) & 0xFFFFull);
+                const int kc = int(((warp < 4 ? tlo : thi) >> sh) & 0xFFFFull);
+                const int g = kb + kc + lane;
+                if (!homo && g < kb + ((kc + 31) & ~31)) s_idx[g] = uint16_t(0xFFFF);
+            } else {
+                const uint64_t tp = tlo * ONES;
+                blo = tp - tlo;                                                    // bases of bins 0..3
+                bhi = thi * ONES - thi + (tp >> 48) * ONES;                        // bases of bins 4..7
+            }
             const uint64_t wlo = shfl64(blo + ilo - lo, warp), whi = shfl64(bhi + ihi - hi, warp);
             // this thread's first slot per bin: warp offset + warp-exclusive count
             const uint64_t ex8 = incl - c8;
@@ -459,10 +492,11 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
             for (int i = 0; i < ITEMS; ++i) {
                 const int b = lb[i];
                 if (b >= 0) {
-                    const int sh = 16 * (b & 3);
-                    const uint64_t word = b < 4 ? plo : phi;
+                    const int kk = PADK ? 7 - b : b;
+                    const int sh = 16 * (kk & 3);
+                    const uint64_t word = kk < 4 ? plo : phi;
                     const int pos = int((word >> sh) & 0xFFFFull);
-                    if (b < 4) plo += 1ull << sh; else phi += 1ull << sh;
+                    if (kk < 4) plo += 1ull << sh; else phi += 1ull << sh;
                     s_idx[pos] = uint16_t((tid + i * TPB) | (b << 12));   // tile index | bin
                 }
             }
@@ -470,20 +504,42 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
         }
         // a homogeneous tile needs no sort: every thread evaluates the elements it binned
         // (slot p = element p), so no thread reads another's writes before the next barrier
-        const int hw = (homo - 1) << 12;
-        // 3. evaluate: sorted slot p -> element j of the stage (warp w takes the
-        //    32-slot chunks w, w + 8, w + 16, w + 24: the expensive high bins at
-        //    the end of the order land on different warps)
+        static_assert(!PADK || TPB / 32 == 8, "one warp per sort key fills that key's padding");
+        const int hw = (PADK ? 7 - (homo - 1) : homo - 1) << 12;   // PADK: bin = 7 - key
+        if constexpr (PADK) {
+            // 3. evaluate the 32-slot chunks of the sorted order, dealt to the warps in
+            //    snake order (w, 15 - w, 16 + w, 31 - w, ...): the costliest chunks come
+            //    first and each round of eight runs opposite to the previous one.  A padded
+            //    order spans up to TILE + 7 * 31 slots; its padding slots (0xFFFF) are skipped.
+            const int nc = homo ? (rem + 31) >> 5 : nchunk;
+            const int up = 15 - 2 * warp, dn = 1 + 2 * warp;
 #pragma unroll 1
-        for (int i = 0; i < ITEMS; ++i) {
-            const int p = tid + i * TPB;
-            if (p < rem) {
-                const int w = homo ? (p | hw) : s_idx[p];
+            for (int c = warp; c < nc; c += (c & 8) ? dn : up) {
+                const int p = (c << 5) + lane;
+                const int w = homo ? (p < rem ? (p | hw) : 0xFFFF) : s_idx[p];
+                if (w == 0xFFFF) continue;
                 const int j = w & 0xFFF;
                 if constexpr (FN == FN_IK) {
                     eval_bin_ik<T>(w >> 12, sv[j], sx[j], s_res[0][j], s_res[NOUT - 1][j]);
                 } else {
                     s_res[0][j] = eval_bin<T, FN>(w >> 12, sv[j], sx[j]);
+                }
+            }
+        } else {
+            // 3. evaluate: sorted slot p -> element j of the stage (warp w takes the
+            //    32-slot chunks w, w + 8, w + 16, w + 24: the expensive high bins at
+            //    the end of the order land on different warps)
+#pragma unroll 1
+            for (int i = 0; i < ITEMS; ++i) {
+                const int p = tid + i * TPB;
+                if (p < rem) {
+                    const int w = homo ? (p | hw) : s_idx[p];
+                    const int j = w & 0xFFF;
+                    if constexpr (FN == FN_IK) {
+                        eval_bin_ik<T>(w >> 12, sv[j], sx[j], s_res[0][j], s_res[NOUT - 1][j]);
+                    } else {
+                        s_res[0][j] = eval_bin<T, FN>(w >> 12, sv[j], sx[j]);
+                    }
                 }
             }
         }

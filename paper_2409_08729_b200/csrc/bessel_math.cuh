@@ -750,9 +750,26 @@ __device__ __forceinline__ T temme_kmu(T mu, T x, T &sum, T &sum1) {
 // node is already O(1) of the k = 0 term (2x sinh^2(h/2) < 0.4), so a term
 // below eps of the sum only occurs past the peak: stop at the first K_{mu+1}
 // term (the wider integrand) below eps of its sum.
-// Returns log K_mu and rho = K_{mu+1} / K_mu.  12-17 nodes on the band.
+// 2 cosh(z) for |z| <= 0.36 by its Taylor series in z^2 (the z^16 term is < 2^-60 of the sum):
+// eight FP64 operations instead of an exp and a reciprocal
 template <typename T>
-__device__ __forceinline__ T trap_kmu(T mu, T x, T &rho) {
+__device__ __forceinline__ T two_cosh_small(T z) {
+    const T z2 = z * z;
+    T p = T(2.0 / 87178291200.0);                                   // 2/14!
+    p = fma(p, z2, T(2.0 / 479001600.0));                           // 2/12!
+    p = fma(p, z2, T(2.0 / 3628800.0));                             // 2/10!
+    p = fma(p, z2, T(2.0 / 40320.0));                               // 2/8!
+    p = fma(p, z2, T(2.0 / 720.0));                                 // 2/6!
+    p = fma(p, z2, T(2.0 / 24.0));                                  // 2/4!
+    p = fma(p, z2, T(1));                                           // 2/2!
+    return fma(p, z2, T(2));
+}
+
+// Returns log K_mu and rho = K_{mu+1} / K_mu.  12-17 nodes on the band.
+// kl (optional): K_mu e^x = (h/2) A, so log K_mu = -x + log kl (callers that
+// fold further factors into one log use it).
+template <typename T>
+__device__ __forceinline__ T trap_kmu(T mu, T x, T &rho, T *kl = nullptr) {
     // f64: h = pi^2 / (42 + 0.8 x) (measured largest admissible step for 2^-53, R14);
     // f32: the error ~ exp(-pi^2 / h) only has to reach ~2^-26: h = pi^2 / (24 + 0.45 x)
     const T h = hc<T>(HC_PI2) * fm_rcp(sizeof(T) == 8 ? fma(T(0.8), x, T(42)) : fma(T(0.45), x, T(24)));
@@ -761,10 +778,15 @@ __device__ __forceinline__ T trap_kmu(T mu, T x, T &rho) {
     const T s1 = a * fma(a2 * T(1.0 / 6), fma(a2 * T(1.0 / 20), fma(a2 * T(1.0 / 42), fma(a2, T(1.0 / 72), T(1)), T(1)), T(1)), T(1));
     const T c = fma(a2, fma(a2 * T(1.0 / 12), fma(a2 * T(1.0 / 30), fma(a2, T(1.0 / 56), T(1)), T(1)), T(1)), T(2));
     // 2 cosh(k nu h) for nu = mu, mu+1 by the recurrence C_{k+1} = c C_k - C_{k-1},
-    // c = 2 cosh(nu h) (forward-stable: the growing solution dominates)
+    // c = 2 cosh(nu h) (forward-stable: the growing solution dominates); |mu h| <= 0.12,
+    // (mu + 1) h <= 1.5 h <= 0.36 on 2 < x (h <= 0.235)
+#if B200_TRAP_EXPCOSH
     const T Em = fm_exp(mu * h), Emi = fm_rcp(Em);
     const T eh = fm_exp(h);
     const T cm = Em + Emi, cp = fma(Em, eh, Emi * fm_rcp(eh));
+#else
+    const T cm = two_cosh_small<T>(mu * h), cp = two_cosh_small<T>((mu + T(1)) * h);
+#endif
     // (a0, a1) = (C_{k-1}, C_k) for order mu, (b0, b1) for mu+1, (x0, x1) = (s_{k-1}, s_k):
     // each trip overwrites the older of every pair with the next value (no register
     // moves in the loop), k = 1 at entry
@@ -787,6 +809,10 @@ __device__ __forceinline__ T trap_kmu(T mu, T x, T &rho) {
         b1 = fma(cp, b0, -b1);
     }
     rho = B * fm_rcp(A);
+    if (kl) {
+        *kl = T(0.5) * h * A;
+        return T(0);   // unused by such callers
+    }
     return -x + fm_log(T(0.5) * h * A);
 }
 
@@ -871,13 +897,15 @@ __device__ __forceinline__ void log_ivkv_trap(T v, T x, T &ri, T &rk) {
     const T mu = v - T(nl);
     const T tox = T(2) * fm_rcp(x);
     T rho;
-    T lk;
+    // K_mu = e^off * kl: off = -x, kl = (h/2) A (trapezoid), off = 0, kl = Temme's sum;
+    // both logs below take kl as a factor (two logs per pair instead of three)
+    T kl;
     if constexpr (TEMME) {
-        T S, S1;
-        lk = temme_kmu<T>(mu, x, S, S1);
-        rho = T(2) * S1 * fm_rcp(x * S);
+        T S1;
+        (void)temme_kmu<T>(mu, x, kl, S1);
+        rho = T(2) * S1 * fm_rcp(x * kl);
     } else {
-        lk = trap_kmu<T>(mu, x, rho);
+        (void)trap_kmu<T>(mu, x, rho, &kl);
     }
     // kp = K_v / K_mu, kn = K_{v+1} / K_mu (one recurrence step past v); the
     // coefficient 2 nu / x advances by one addition of 2/x per step
@@ -890,27 +918,35 @@ __device__ __forceinline__ void log_ivkv_trap(T v, T x, T &ri, T &rk) {
         kp = kn;
     }
     // after the loop: kp = K_{v+1}/K_mu, km = K_v/K_mu
-    const int M = sizeof(T) == 8 ? int(fmin(T(12) + x, fma(T(0.55), x, T(20)))) + 1
-                                 : int(fmin(T(6) + x, fma(T(0.5), x, T(12)))) + 1;
+    // M rounded up to a multiple of 4 (four steps per trip, no remainder; more steps only
+    // shrink the start error; |y| grows by at most (2 (v + M + 3) / x)^3 < 1e24 over the
+    // bounds of DESIGN.md §5: still far inside the double / float range)
+    const int M = ((sizeof(T) == 8 ? int(fmin(T(12) + x, fma(T(0.55), x, T(20)))) + 1
+                                   : int(fmin(T(6) + x, fma(T(0.5), x, T(12)))) + 1) + 3) & ~3;
     T y1 = T(0), y0 = T(1);                 // y_{v+k+1}, y_{v+k}
     // coefficient b = 2 (v + k) / x, stepped down by one subtraction of 2/x per step
-    // (<= 37 roundings: relative error < 1e-14 in b, far inside the ratio's tolerance;
+    // (<= 40 roundings: relative error < 1e-14 in b, far inside the ratio's tolerance;
     // a multiply per step, or an int -> T conversion (I2F.F64), cost more)
     T b = (v + T(M)) * tox;
-#pragma unroll 2
-    for (int k = M; k >= 1; --k) {
-        const T y = fma(b, y0, y1);
+#pragma unroll 1
+    for (int k = M; k >= 4; k -= 4) {       // the two values swap roles each step (no moves)
+        y1 = fma(b, y0, y1);
         b -= tox;
-        y1 = y0;
-        y0 = y;
+        y0 = fma(b, y1, y0);
+        b -= tox;
+        y1 = fma(b, y0, y1);
+        b -= tox;
+        y0 = fma(b, y1, y0);
+        b -= tox;
     }
-    // r = y1 / y0;  1 / (I_v K_mu) = x (K_{v+1} + r K_v) / K_mu
-    rk = nl == 0 ? lk : lk + fm_log(km);
+    // y0 = y_v, y1 = y_{v+1}: r = y1 / y0;  1 / (I_v K_mu) = x (K_{v+1} + r K_v) / K_mu
+    const T off = TEMME ? T(0) : -x;
+    rk = off + fm_log(kl * km);
     if constexpr (sizeof(T) == 8) {
-        ri = -lk - fm_log(x * fma(km, y1, kp * y0) * fm_rcp(y0));
+        ri = -off - fm_log(kl * x * fma(km, y1, kp * y0) * fm_rcp(y0));
     } else {
         // f32: kp y0 can pass FLT_MAX near x = 0.1 (~1e27 * 1e17); take the ratio first
-        ri = -lk - fm_log(x * fma(km, y1 * fm_rcp(y0), kp));
+        ri = -off - fm_log(kl * x * fma(km, y1 * fm_rcp(y0), kp));
     }
 }
 

@@ -22,7 +22,8 @@ BOXES = {
 
 def main():
     lib = sys.argv[1]
-    names = [a for a in sys.argv[2:] if not a.startswith("--")]
+    args = sys.argv[2:]
+    names = [a for i, a in enumerate(args) if not a.startswith("--") and not (i and args[i - 1] == "--n")]
     n = int(sys.argv[sys.argv.index("--n") + 1]) if "--n" in sys.argv else 4_000_000
     L = ctypes.CDLL(lib)
     L.b200_log_ivkv_f64.argtypes = [ctypes.c_void_p] * 4 + [ctypes.c_int64, ctypes.c_void_p]
