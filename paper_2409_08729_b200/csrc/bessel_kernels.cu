@@ -115,13 +115,15 @@ __device__ __forceinline__ int bin_of(T v, T x) {
         hvs = __float_as_uint(v);
     }
     const uint32_t hv = hvs & 0x7FFFFFFFu;
-    if (hx - LO > HI - LO) return BIN_SLOW;                             // x outside the range (or <= 0, NaN)
-    if (hv > HI) return BIN_SLOW;                                       // |v| above the range, inf, NaN
-    if ((FN == FN_I || FN == FN_IK) && hvs != hv) return BIN_SLOW;     // v < 0 (or -0.0: handled there)
+    // x outside the range (or <= 0, NaN), |v| above it (inf, NaN), v < 0 for I (-0.0 is
+    // handled there): one predicate and a final select, no early-return branches
+    const bool slow = (hx - LO > HI - LO) | (hv > HI) | ((FN == FN_I || FN == FN_IK) & (hvs != hv));
+    int e;
     if constexpr (sizeof(T) == 8)
-        return select_eval_hw(fabs(v), x, hv, hx, (FN == FN_I) ? B200_HW_X8 : B200_HW_X2);
+        e = select_eval_hw(fabs(v), x, hv, hx, (FN == FN_I) ? B200_HW_X8 : B200_HW_X2);
     else
-        return select_eval_f32(fabsf(v), x, hv, hx, (FN == FN_I) ? B200_F32_X8 : B200_F32_X2);
+        e = select_eval_f32(fabsf(v), x, hv, hx, (FN == FN_I) ? B200_F32_X8 : B200_F32_X2);
+    return slow ? BIN_SLOW : e;
 }
 
 // The slow bin: IEEE special cases, then the full-range (SAFE) evaluation.
@@ -505,7 +507,7 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
         // a homogeneous tile needs no sort: every thread evaluates the elements it binned
         // (slot p = element p), so no thread reads another's writes before the next barrier
         static_assert(!PADK || TPB / 32 == 8, "one warp per sort key fills that key's padding");
-        const int hw = (PADK ? 7 - (homo - 1) : homo - 1) << 12;   // PADK: bin = 7 - key
+        const int hw = (PADK ? 7 - (homo - 1) : homo - 1) << 12;   // the tile's one bin (PADK: 7 - key)
         if constexpr (PADK) {
             // 3. evaluate the 32-slot chunks of the sorted order, dealt to the warps in
             //    snake order (w, 15 - w, 16 + w, 31 - w, ...): the costliest chunks come

@@ -95,9 +95,16 @@ __device__ __forceinline__ uint32_t hiw(double a) { return uint32_t(__double2hii
 // hardware log2 (MUFU.LG2, fp32) and re-evaluated in double only inside a
 // 1e-4 guard band (and beyond the fp32 range), so the result equals the
 // double-precision predicate.
+// log2 by MUFU.LG2 with denormals flushed (no range fix-up instructions): x > 59 here,
+// and a v that flushes to 0 gives -inf, i.e. "mu" -- as the exact predicate does
+__device__ __forceinline__ float lg2_ftz(float a) {
+    float r;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(a));
+    return r;
+}
 __device__ __forceinline__ bool mu_edge(double v, double x, uint32_t hx) {
     if (hx <= B200_HW_X1E30) {
-        const float lx = __log2f(float(x)), lv = __log2f(float(v));
+        const float lx = lg2_ftz(float(x)), lv = lg2_ftz(float(v));
         const float d = 0.5113f * lx + 1.14535832f - lv;   // 0.7939 / ln 2 = 1.14535832
         if (fabsf(d) > 1e-4f) return d > 0.0f;
     }
@@ -792,10 +799,19 @@ __device__ __forceinline__ T trap_kmu(T mu, T x, T &rho, T *kl = nullptr) {
     // moves in the loop), k = 1 at entry
     T a0 = T(2), a1 = cm, b0 = T(2), b1 = cp;
     T A = T(1), B = T(1), x0 = T(0), x1 = s1;
-    const T m2x = T(-2) * x;
+    // f64: the node exponents -2x s_k^2 are formed scaled by 64/ln2 for fm_exp_prescaled
+    // (a relative error |y| 2^-52 in a node of size e^y: < 2^-53 of the sum, R14)
+    const T m2x = sizeof(T) == 8 ? T(-2.0 * 92.33248261689366) * x : T(-2) * x;
     for (int k = 1; k < 64; k += 2) {     // nodes k, k+1 per trip, stop test on the second
         x0 = fma(c, x1, -x0);                                           // s_{k+1}
-        const T e1 = fm_exp_nc(m2x * x1 * x1), e2 = fm_exp_nc(m2x * x0 * x0);
+        T e1, e2;
+        if constexpr (sizeof(T) == 8) {
+            e1 = fm_exp_prescaled(m2x * x1 * x1);
+            e2 = fm_exp_prescaled(m2x * x0 * x0);
+        } else {
+            e1 = fm_exp_nc(m2x * x1 * x1);
+            e2 = fm_exp_nc(m2x * x0 * x0);
+        }
         a0 = fma(cm, a1, -a0);                                          // C_{k+1}
         b0 = fma(cp, b1, -b0);
         A = fma(e1, a1, A);
@@ -1036,7 +1052,7 @@ __device__ __forceinline__ int select_eval(double v, double x, uint32_t hw_split
 // <= C (exact for float a), each "a >= rho_K" bits(a) >= bits(rho_K) -- no conversion
 // of the inputs to double (tables.h B200_F32_*; R3).
 __device__ __forceinline__ bool mu_edge_f32(float v, float x) {
-    const float d = 0.5113f * __log2f(x) + 1.14535832f - __log2f(v);   // 0.7939 / ln 2
+    const float d = 0.5113f * lg2_ftz(x) + 1.14535832f - lg2_ftz(v);   // 0.7939 / ln 2
     if (fabsf(d) > 1e-4f) return d > 0.0f;
     return 0.5113 * log(double(x)) + 0.7939 > log(double(v));         // guard band: the double predicate
 }

@@ -35,6 +35,7 @@ struct FmConst {
     double exp_inv, exp_chi, exp_clo;    // 64/ln2; ln2/64 = chi (33 significant bits) + clo
     double exp_c5, exp_c4, exp_c3;       // 1/120, 1/24, 1/6
     double ln2_lo20, exp_clo20;          // remainders of the 21-significant-bit splits below
+    double exp_ln2o64;                   // ln2/64 (fm_exp_prescaled)
 };
 static __constant__ FmConst c_fm = {
     -1.0 / 6.0, 0.2, 1.0 / 3.0,
@@ -42,6 +43,7 @@ static __constant__ FmConst c_fm = {
     92.33248261689366, 0.010830424695086549, 1.162596423439437e-12,
     1.0 / 120.0, 1.0 / 24.0, 1.0 / 6.0,
     -1.904654299957768e-09, -2.9760223436840126e-11,
+    0.010830424696249145,
 };
 
 #ifndef B200_IMM
@@ -151,6 +153,25 @@ __device__ __forceinline__ double fm_log(double a) {
     const double l = fma(ed, c_fm.ln2_lo, tlo);
 #endif
     return h + (r + fma(r * r, p, l));
+}
+
+// exp(y) from yp = y * 64/ln2, already scaled by the caller (who folds the factor into a
+// product it forms anyway), -65000 <= yp <= 0: the reduction is yp - round(yp), exact,
+// and the 64/ln2 factor needs no register.  yp's own rounding (~2 ulp) is an absolute
+// error |y| 2^-52 in the exponent, i.e. a relative error |y| 2^-52 of the result.
+__device__ __forceinline__ double fm_exp_prescaled(double yp) {
+    constexpr double SHIFT = 6755399441055744.0;               // 1.5 * 2^52: round-to-int (immediate)
+    double kd = yp + SHIFT;
+    const int k = __double2loint(kd);
+    kd -= SHIFT;
+    const double r = (yp - kd) * c_fm.exp_ln2o64;              // |r| <= ln2/128
+    double p = fma(r, IMM_EXP_C5, IMM_EXP_C4);
+    p = fma(p, r, c_fm.exp_c3);
+    p = fma(p, r, 0.5);
+    p = fma(p, r * r, r);
+    const double2 T = __ldg(&g_exptab[k & (B200_EXP_TAB_N - 1)]);
+    const double res = T.x + fma(T.x, p, T.y);
+    return __hiloint2double(__double2hiint(res) + ((k >> 6) << 20), __double2loint(res));
 }
 
 // exp(y) for -708 <= y <= 709 (result normal); y < -708 is clamped (callers
