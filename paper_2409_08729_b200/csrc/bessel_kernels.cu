@@ -68,6 +68,9 @@ constexpr int BIN_SLOW = 7;           // out-of-range / special inputs (slow_eva
 #ifndef B200_C32
 #define B200_C32 0                    // 1: 32-bit bin-counter increments
 #endif
+#ifndef B200_PLOOP
+#define B200_PLOOP 1                  // 1: the unpadded evaluation loop runs on the slot index (0: element counter)
+#endif
 #ifndef B200_IFCHAIN
 #define B200_IFCHAIN 0                // 1: fused pass dispatches the cheap bins by compares
 #endif
@@ -513,11 +516,13 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
             //    snake order (w, 15 - w, 16 + w, 31 - w, ...): the costliest chunks come
             //    first and each round of eight runs opposite to the previous one.  A padded
             //    order spans up to TILE + 7 * 31 slots; its padding slots (0xFFFF) are skipped.
-            const int nc = homo ? (rem + 31) >> 5 : nchunk;
-            const int up = 15 - 2 * warp, dn = 1 + 2 * warp;
+            //    On slot indices p = 32 c + lane the snake step needs neither the warp nor
+            //    the lane: c -> c ^ 15 (16m + w -> 16m + 15 - w) then c -> (c ^ 15) + 16,
+            //    i.e. p -> (p ^ 480) + ((p & 256) << 1), starting at p = tid (no SR_TID
+            //    re-reads inside the loop).
+            const int np = (homo ? (rem + 31) >> 5 : nchunk) << 5;
 #pragma unroll 1
-            for (int c = warp; c < nc; c += (c & 8) ? dn : up) {
-                const int p = (c << 5) + lane;
+            for (int p = tid; p < np; p = (p ^ 480) + ((p & 256) << 1)) {
                 const int w = homo ? (p < rem ? (p | hw) : 0xFFFF) : s_idx[p];
                 if (w == 0xFFFF) continue;
                 const int j = w & 0xFFF;
@@ -531,6 +536,18 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
             // 3. evaluate: sorted slot p -> element j of the stage (warp w takes the
             //    32-slot chunks w, w + 8, w + 16, w + 24: the expensive high bins at
             //    the end of the order land on different warps)
+#if B200_PLOOP
+#pragma unroll 1
+            for (int p = tid; p < rem; p += TPB) {   // the slot index is the loop variable
+                const int w = homo ? (p | hw) : s_idx[p];
+                const int j = w & 0xFFF;
+                if constexpr (FN == FN_IK) {
+                    eval_bin_ik<T>(w >> 12, sv[j], sx[j], s_res[0][j], s_res[NOUT - 1][j]);
+                } else {
+                    s_res[0][j] = eval_bin<T, FN>(w >> 12, sv[j], sx[j]);
+                }
+            }
+#else
 #pragma unroll 1
             for (int i = 0; i < ITEMS; ++i) {
                 const int p = tid + i * TPB;
@@ -544,6 +561,7 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
                     }
                 }
             }
+#endif
         }
         __syncthreads();
         // 4. store
