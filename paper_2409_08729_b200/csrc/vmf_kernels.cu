@@ -22,6 +22,29 @@ extern std::atomic<int64_t> g_launches;   // defined in bessel_kernels.cu
 int set_err(int code, const char *msg);    // bessel_kernels.cu: per-thread last-error string
 int cuda_err(cudaError_t e, const char *where);
 
+// Programmatic dependent launch: the column-sum partial -> reduce -> fit chain is
+// launched with cudaLaunchAttributeProgrammaticStreamSerialization, so a dependent
+// grid is scheduled while its producer drains and waits at griddepcontrol.wait for
+// the producer's completion (memory visible); launched without the attribute, both
+// instructions are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" :::); }
+
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 constexpr int CS_TPB = 256;
 #ifndef B200_CS_ROWS
 #define B200_CS_ROWS 8
@@ -55,6 +78,7 @@ __global__ void __launch_bounds__(CS_TPB) colsum_partial_kernel(const T *__restr
                                                                 double *__restrict__ part) {
     constexpr int VN = VEC ? VecOf<T>::N : 1;
     constexpr int CW = CS_TPB * VN;
+    pdl_launch_dependents();   // the reduce kernel may be scheduled now; it waits for this grid
     const int64_t c0 = int64_t(blockIdx.x) * CW + int64_t(threadIdx.x) * VN;
     const int64_t r0 = int64_t(blockIdx.y) * rows_per;
     int64_t r1 = r0 + rows_per;
@@ -106,6 +130,8 @@ __global__ void __launch_bounds__(32 * CR_WARPS) colsum_reduce_kernel(const doub
                                                                      int accumulate, int with_count, double n_rows) {
     __shared__ double sh[CR_WARPS][32];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    pdl_wait();                // the partials of the preceding grid are complete and visible
+    pdl_launch_dependents();
     if (with_count && blockIdx.x == 0 && threadIdx.x == 0) colsum[d] = accumulate ? colsum[d] + n_rows : n_rows;
     for (int64_t c0 = int64_t(blockIdx.x) * 32; c0 < d; c0 += int64_t(gridDim.x) * 32) {
         const int64_t j = c0 + lane;
@@ -165,6 +191,7 @@ __global__ void __launch_bounds__(FIT_TPB) vmf_fit_kernel(const double *__restri
                                                           int64_t d, double *__restrict__ mu,
                                                           double *__restrict__ stats) {
     fm_tables_init();
+    pdl_wait();                // the column sums of the preceding grid (reduce / all-reduce) are visible
     __shared__ double s_red[FIT_TPB / 32];
     __shared__ double s_rbar;
     __shared__ double s_l[2];
@@ -371,10 +398,12 @@ static int colsum_impl(const T *X, int64_t n, int64_t d, int64_t ld, double *col
     else
         colsum_partial_kernel<T, false><<<grid, CS_TPB, 0, s>>>(X, n, d, ld, rows_per, part);
     const int64_t rb = (d + 31) / 32;
-    colsum_reduce_kernel<<<unsigned(rb < 4096 ? rb : 4096), 32 * CR_WARPS, 0, s>>>(part, nslab, d, colsum, accumulate,
-                                                                                 with_count, double(n));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_err(e, "vmf colsum partial launch");
+    e = launch_pdl(colsum_reduce_kernel, dim3(unsigned(rb < 4096 ? rb : 4096)), dim3(32 * CR_WARPS), s,
+                   (const double *)part, nslab, d, colsum, accumulate, with_count, double(n));
     g_launches.fetch_add(2, std::memory_order_relaxed);
-    return cuda_err(cudaGetLastError(), "vmf colsum launch");
+    return cuda_err(e, "vmf colsum reduce launch");
 }
 
 static int fit_from_colsum_impl(const double *colsum, int64_t n_total, int64_t d, double *mu, double *stats,
@@ -382,9 +411,9 @@ static int fit_from_colsum_impl(const double *colsum, int64_t n_total, int64_t d
     if (d < 2 || !colsum || !mu || !stats) return set_err(B200_ERR_INVALID_ARGUMENT, "vmf_fit: d < 2 or null pointer");
     if (n_total < 0) return set_err(B200_ERR_INVALID_ARGUMENT, "vmf_fit: n_total < 0");
     // n_total == 0: the row count is read from colsum[d] (b200_vmf_colsum_* with with_count)
-    vmf_fit_kernel<<<1, FIT_TPB, 0, s>>>(colsum, n_total, d, mu, stats);
+    const cudaError_t e = launch_pdl(vmf_fit_kernel, dim3(1), dim3(FIT_TPB), s, colsum, n_total, d, mu, stats);
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    return cuda_err(cudaGetLastError(), "vmf_fit_kernel launch");
+    return cuda_err(e, "vmf_fit_kernel launch");
 }
 
 }  // namespace b200
