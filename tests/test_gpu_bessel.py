@@ -302,6 +302,55 @@ def test_fused_ivkv_against_oracle(B, case):
     assert oracle.rel_err(gk[ok], rk).max() <= TOL64
 
 
+# one (v, x) box per evaluation bin of the fused pass (R12/R13, Table 1 predicates)
+_BIN_BOXES = {
+    "mu": ((0.0, 10.0), (40.0, 90.0)),
+    "u6": ((300.0, 800.0), (1.0, 100.0)),
+    "u8": ((120.0, 250.0), (1.0, 100.0)),
+    "u10": ((65.0, 100.0), (1.0, 60.0)),
+    "u13": ((14.0, 50.0), (1.0, 19.0)),
+    "temme": ((0.5, 12.0), (0.1, 2.0)),
+    "trapezoid": ((0.5, 12.0), (2.5, 19.0)),
+    "slow": ((0.0, 5.0), (1e-150, 1e-145)),      # x below the f64 operating range (R13)
+}
+
+
+@pytest.mark.timeout(600)
+def test_fused_every_bin_in_every_tile(B):
+    """Mixed tiles of the fused f64 pass (costliest-first order, bins padded to 32-slot
+    chunks, snake dealing): every tile holds all eight bins, with per-bin
+    counts of 0, 1, 31, 32, 33 and more (no padding, 31 padding slots, a bin that fills
+    whole chunks), shuffled, plus a ragged last tile; both results against the oracle."""
+    rng = np.random.default_rng(41)
+    counts = [[32, 1, 31, 33, 64, 5, 17, 3], [0, 200, 0, 0, 1, 0, 100, 0], [1, 1, 1, 1, 1, 1, 1, 1],
+              [192, 0, 64, 0, 96, 31, 33, 32], [7, 40, 9, 300, 2, 11, 5, 1]]
+    names = list(_BIN_BOXES)
+    vs, xs = [], []
+    for row in counts + [[9, 9, 9, 9, 9, 9, 9, 9]]:          # the last tile is ragged (72 pairs)
+        tv, tx = [], []
+        for nm, c in zip(names, row):
+            (v0, v1), (x0, x1) = _BIN_BOXES[nm]
+            tv.append(rng.uniform(v0, v1, c))
+            tx.append(np.exp(rng.uniform(math.log(x0), math.log(x1), c)) if nm == "slow" else rng.uniform(x0, x1, c))
+        tv, tx = np.concatenate(tv), np.concatenate(tx)
+        if len(vs) < len(counts):                  # fill the full tiles to 1536 pairs with mu pairs
+            k = 1536 - tv.size
+            tv = np.concatenate([tv, rng.uniform(0.0, 10.0, k)])
+            tx = np.concatenate([tx, rng.uniform(40.0, 90.0, k)])
+        perm = rng.permutation(tv.size)
+        vs.append(tv[perm])
+        xs.append(tx[perm])
+    v, x = np.concatenate(vs), np.concatenate(xs)
+    assert v.size == 5 * 1536 + 72
+    gi, gk = _run_ivkv(B, v, x)
+    assert np.all(np.isfinite(gi)) and np.all(np.isfinite(gk))
+    ri, rk = oracle.log_iv(v, x), oracle.log_kv(v, x)
+    ei, ek = oracle.rel_err(gi, ri), oracle.rel_err(gk, rk)
+    i, k = int(np.argmax(ei)), int(np.argmax(ek))
+    assert ei[i] <= TOL64, f"log I err {ei[i]:.3e} at v={v[i]!r} x={x[i]!r}"
+    assert ek[k] <= TOL64, f"log K err {ek[k]:.3e} at v={v[k]!r} x={x[k]!r}"
+
+
 def test_fused_ivkv_f32_and_host(B):
     v, x = workloads.small_case(10_000, seed=36)
     gi, gk = _run_ivkv(B, v, x, torch.float32)
