@@ -68,6 +68,12 @@ constexpr int BIN_SLOW = 7;           // out-of-range / special inputs (slow_eva
 #ifndef B200_C32
 #define B200_C32 0                    // 1: 32-bit bin-counter increments
 #endif
+#ifndef B200_SADDR
+#define B200_SADDR 1                  // 1: the fused f64 loop addresses the stage by 32-bit shared addresses
+#endif
+#ifndef B200_SADDR2
+#define B200_SADDR2 1                 // 1: the same in the other kernels' evaluation loop
+#endif
 #ifndef B200_PLOOP
 #define B200_PLOOP 1                  // 1: the unpadded evaluation loop runs on the slot index (0: element counter)
 #endif
@@ -248,6 +254,39 @@ static_assert(ITEMS <= 7, "8-bit warp-level bin counters hold at most 255 = 32 *
 // (loads) or a bulk group (stores).  Pointers that are only 8-byte aligned
 // fall back to per-thread cp.async (LDGSTS) loads and plain stores.
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return uint32_t(__cvta_generic_to_shared(p)); }
+// 32-bit shared-memory accesses (B200_SADDR): volatile, so they keep their order
+// relative to the barriers and to each other
+__device__ __forceinline__ uint32_t opaque_u32(uint32_t a) {
+    asm volatile("mov.b32 %0, %0;" : "+r"(a));
+    return a;
+}
+__device__ __forceinline__ double lds_f64(uint32_t a) {
+    double r;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(r) : "r"(a) : "memory");
+    return r;
+}
+__device__ __forceinline__ void sts_f64(uint32_t a, double v) {
+    asm volatile("st.shared.f64 [%0], %1;" ::"r"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+    float r;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(r) : "r"(a) : "memory");
+    return r;
+}
+__device__ __forceinline__ void sts_f32(uint32_t a, float v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+template <typename T> __device__ __forceinline__ T lds_t(uint32_t a) {
+    if constexpr (sizeof(T) == 8) return lds_f64(a); else return lds_f32(a);
+}
+template <typename T> __device__ __forceinline__ void sts_t(uint32_t a, T v) {
+    if constexpr (sizeof(T) == 8) sts_f64(a, v); else sts_f32(a, v);
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+    unsigned short r;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(r) : "r"(a) : "memory");
+    return r;
+}
 __device__ __forceinline__ void mbar_init(uint64_t *bar) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -522,7 +561,21 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
             //    re-reads inside the loop).
             const int np = (homo ? (rem + 31) >> 5 : nchunk) << 5;
 #pragma unroll 1
+#if B200_SADDR
+            // 32-bit shared addresses held in registers the compiler cannot re-derive:
+            // without this it recomputes the shared window (S2R SR_CgaCtaId, LEA) per element
+            const uint32_t a_st = opaque_u32(smem_u32(sv)), a_ix = opaque_u32(smem_u32(s_idx));
+#endif
             for (int p = tid; p < np; p = (p ^ 480) + ((p & 256) << 1)) {
+#if B200_SADDR
+                const int w = homo ? (p < rem ? (p | hw) : 0xFFFF) : int(lds_u16(a_ix + 2 * p));
+                if (w == 0xFFFF) continue;
+                const uint32_t a = a_st + sizeof(T) * (w & 0xFFF);
+                T ri, rk;
+                eval_bin_ik<T>(w >> 12, lds_t<T>(a), lds_t<T>(a + sizeof(T) * TILE), ri, rk);
+                sts_t<T>(a, ri);
+                sts_t<T>(a + sizeof(T) * TILE, rk);
+#else
                 const int w = homo ? (p < rem ? (p | hw) : 0xFFFF) : s_idx[p];
                 if (w == 0xFFFF) continue;
                 const int j = w & 0xFFF;
@@ -531,14 +584,30 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
                 } else {
                     s_res[0][j] = eval_bin<T, FN>(w >> 12, sv[j], sx[j]);
                 }
+#endif
             }
         } else {
             // 3. evaluate: sorted slot p -> element j of the stage (warp w takes the
             //    32-slot chunks w, w + 8, w + 16, w + 24: the expensive high bins at
             //    the end of the order land on different warps)
 #if B200_PLOOP
+#if B200_SADDR2
+            const uint32_t a_st = opaque_u32(smem_u32(sv)), a_ix = opaque_u32(smem_u32(s_idx));
+#endif
 #pragma unroll 1
             for (int p = tid; p < rem; p += TPB) {   // the slot index is the loop variable
+#if B200_SADDR2
+                const int w = homo ? (p | hw) : int(lds_u16(a_ix + 2 * p));
+                const uint32_t a = a_st + sizeof(T) * (w & 0xFFF);
+                if constexpr (FN == FN_IK) {
+                    T ri, rk;
+                    eval_bin_ik<T>(w >> 12, lds_t<T>(a), lds_t<T>(a + sizeof(T) * TILE), ri, rk);
+                    sts_t<T>(a, ri);
+                    sts_t<T>(a + sizeof(T) * TILE, rk);
+                } else {
+                    sts_t<T>(a, eval_bin<T, FN>(w >> 12, lds_t<T>(a), lds_t<T>(a + sizeof(T) * TILE)));
+                }
+#else
                 const int w = homo ? (p | hw) : s_idx[p];
                 const int j = w & 0xFFF;
                 if constexpr (FN == FN_IK) {
@@ -546,6 +615,7 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
                 } else {
                     s_res[0][j] = eval_bin<T, FN>(w >> 12, sv[j], sx[j]);
                 }
+#endif
             }
 #else
 #pragma unroll 1
