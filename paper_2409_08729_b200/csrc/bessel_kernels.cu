@@ -157,58 +157,58 @@ __device__ __noinline__ T slow_eval(T v, T x) {
 }
 
 template <typename T, int FN>
-__device__ __forceinline__ T eval_bin(int bin, T v, T x) {
+__device__ __forceinline__ T eval_bin(int bin, T v, T x, uint32_t tab) {
 #ifdef B200_EVAL_NOP
     if (bin != BIN_SLOW) return v + x;   // experiment only: measures the tile machinery alone
 #endif
     if (FN == FN_I) {
         switch (bin) {
-            case E_MU: return log_bessel_mu<T, false, false>(v, x);
-            case E_UA: return log_bessel_u<T, false, KUs<T>::A, false>(v, x);
-            case E_UB: return log_bessel_u<T, false, KUs<T>::B, false>(v, x);
-            case E_UC: return log_bessel_u<T, false, KUs<T>::C, false>(v, x);
-            case E_U13: return log_bessel_u<T, false, KUs<T>::D, false>(v, x);
+            case E_MU: return log_bessel_mu<T, false, false>(v, x, tab);
+            case E_UA: return log_bessel_u<T, false, KUs<T>::A, false>(v, x, tab);
+            case E_UB: return log_bessel_u<T, false, KUs<T>::B, false>(v, x, tab);
+            case E_UC: return log_bessel_u<T, false, KUs<T>::C, false>(v, x, tab);
+            case E_U13: return log_bessel_u<T, false, KUs<T>::D, false>(v, x, tab);
             case E_FB_A:
-            case E_FB_B: return log_iv_series<T, false>(v, x);
+            case E_FB_B: return log_iv_series<T, false>(v, x, tab);
             default: return slow_eval<T, FN>(v, x);
         }
     }
     const T av = fabs(v);
     switch (bin) {
-        case E_MU: return log_bessel_mu<T, true, false>(av, x);
-        case E_UA: return log_bessel_u<T, true, KUs<T>::A, false>(av, x);
-        case E_UB: return log_bessel_u<T, true, KUs<T>::B, false>(av, x);
-        case E_UC: return log_bessel_u<T, true, KUs<T>::C, false>(av, x);
-        case E_U13: return log_bessel_u<T, true, KUs<T>::D, false>(av, x);
+        case E_MU: return log_bessel_mu<T, true, false>(av, x, tab);
+        case E_UA: return log_bessel_u<T, true, KUs<T>::A, false>(av, x, tab);
+        case E_UB: return log_bessel_u<T, true, KUs<T>::B, false>(av, x, tab);
+        case E_UC: return log_bessel_u<T, true, KUs<T>::C, false>(av, x, tab);
+        case E_U13: return log_bessel_u<T, true, KUs<T>::D, false>(av, x, tab);
         case E_FB_A:
-        case E_FB_B: return FN == FN_K_PAPER ? log_kv_integral_paper<T>(av, x) : log_kv_fallback<T, false>(av, x);
+        case E_FB_B: return FN == FN_K_PAPER ? log_kv_integral_paper<T>(av, x) : log_kv_fallback<T, false>(av, x, tab);
         default: return slow_eval<T, FN>(v, x);
     }
 }
 
 // Fused I + K: both results of one element (bins as for K, v >= 0 or slow).
 template <typename T>
-__device__ __forceinline__ void eval_bin_ik(int bin, T v, T x, T &ri, T &rk) {
+__device__ __forceinline__ void eval_bin_ik(int bin, T v, T x, T &ri, T &rk, uint32_t tab) {
 #ifdef B200_EVAL_NOP
     if (bin != BIN_SLOW) { ri = v + x; rk = v - x; return; }
 #endif
 #if B200_IFCHAIN
     // the cheap bins by compare-and-branch (warp-uniform after the sort); no jump table
-    if (bin == E_MU) { log_bessel_mu_ik<T>(v, x, ri, rk); return; }
-    if (bin == E_UA) { log_bessel_u_ik<T, KUs<T>::A>(v, x, ri, rk); return; }
-    if (bin == E_UB) { log_bessel_u_ik<T, KUs<T>::B>(v, x, ri, rk); return; }
-    if (bin == E_UC) { log_bessel_u_ik<T, KUs<T>::C>(v, x, ri, rk); return; }
-    if (bin == E_U13) { log_bessel_u_ik<T, KUs<T>::D>(v, x, ri, rk); return; }
+    if (bin == E_MU) { log_bessel_mu_ik<T>(v, x, ri, rk, tab); return; }
+    if (bin == E_UA) { log_bessel_u_ik<T, KUs<T>::A>(v, x, ri, rk, tab); return; }
+    if (bin == E_UB) { log_bessel_u_ik<T, KUs<T>::B>(v, x, ri, rk, tab); return; }
+    if (bin == E_UC) { log_bessel_u_ik<T, KUs<T>::C>(v, x, ri, rk, tab); return; }
+    if (bin == E_U13) { log_bessel_u_ik<T, KUs<T>::D>(v, x, ri, rk, tab); return; }
 #endif
     switch (bin) {
-        case E_MU: log_bessel_mu_ik<T>(v, x, ri, rk); break;
-        case E_UA: log_bessel_u_ik<T, KUs<T>::A>(v, x, ri, rk); break;
-        case E_UB: log_bessel_u_ik<T, KUs<T>::B>(v, x, ri, rk); break;
-        case E_UC: log_bessel_u_ik<T, KUs<T>::C>(v, x, ri, rk); break;
-        case E_U13: log_bessel_u_ik<T, KUs<T>::D>(v, x, ri, rk); break;
+        case E_MU: log_bessel_mu_ik<T>(v, x, ri, rk, tab); break;
+        case E_UA: log_bessel_u_ik<T, KUs<T>::A>(v, x, ri, rk, tab); break;
+        case E_UB: log_bessel_u_ik<T, KUs<T>::B>(v, x, ri, rk, tab); break;
+        case E_UC: log_bessel_u_ik<T, KUs<T>::C>(v, x, ri, rk, tab); break;
+        case E_U13: log_bessel_u_ik<T, KUs<T>::D>(v, x, ri, rk, tab); break;
         case E_FB_B:   // 2 < x <= 30
 #ifndef B200_IK_SERIES   // experiment switch: the power series for I on this band too
-            log_ivkv_trap<T>(v, x, ri, rk);   // I from the K values (Wronskian + Miller ratio)
+            log_ivkv_trap<T>(v, x, ri, rk, tab);   // I from the K values (Wronskian + Miller ratio)
             break;
 #endif
         case E_FB_A:   // x <= 2
@@ -218,12 +218,12 @@ __device__ __forceinline__ void eval_bin_ik(int bin, T v, T x, T &ri, T &rk) {
             // error (R1).  f32: from x = 0.1, where the Miller values stay below
             // ~(2 (v + M) / x)^M < 2e18 and K_{v+1} / K_mu < 1e27 (FLT_MAX 3.4e38)
             if (x >= T(sizeof(T) == 8 ? 1e-6 : 0.1) && x <= T(2) && v >= T(0.5)) {
-                log_ivkv_trap<T, true>(v, x, ri, rk);   // Temme K values, Wronskian + Miller ratio
+                log_ivkv_trap<T, true>(v, x, ri, rk, tab);   // Temme K values, Wronskian + Miller ratio
                 break;
             }
 #endif
-            ri = log_iv_series<T, false>(v, x);
-            rk = log_kv_fallback<T, false>(v, x);
+            ri = log_iv_series<T, false>(v, x, tab);
+            rk = log_kv_fallback<T, false>(v, x, tab);
             break;
         default:
             ri = slow_eval<T, FN_I>(v, x);
@@ -368,6 +368,8 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t ntiles = (n + TILE - 1) / TILE;
     fm_tables_init();   // the f64 log table (the f32 kernels use it in the double K recurrence)
+    // its shared address, computed once and held where the compiler cannot re-derive it
+    const uint32_t tab = opaque_u32(logtab_addr());
     auto tile_rem = [&](int64_t t) { return int(n - t * TILE < TILE ? n - t * TILE : TILE); };
 
     // stage tile t into buffer (t / gridDim.x) & 1
@@ -572,7 +574,7 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
                 if (w == 0xFFFF) continue;
                 const uint32_t a = a_st + sizeof(T) * (w & 0xFFF);
                 T ri, rk;
-                eval_bin_ik<T>(w >> 12, lds_t<T>(a), lds_t<T>(a + sizeof(T) * TILE), ri, rk);
+                eval_bin_ik<T>(w >> 12, lds_t<T>(a), lds_t<T>(a + sizeof(T) * TILE), ri, rk, tab);
                 sts_t<T>(a, ri);
                 sts_t<T>(a + sizeof(T) * TILE, rk);
 #else
@@ -580,9 +582,9 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
                 if (w == 0xFFFF) continue;
                 const int j = w & 0xFFF;
                 if constexpr (FN == FN_IK) {
-                    eval_bin_ik<T>(w >> 12, sv[j], sx[j], s_res[0][j], s_res[NOUT - 1][j]);
+                    eval_bin_ik<T>(w >> 12, sv[j], sx[j], s_res[0][j], s_res[NOUT - 1][j], tab);
                 } else {
-                    s_res[0][j] = eval_bin<T, FN>(w >> 12, sv[j], sx[j]);
+                    s_res[0][j] = eval_bin<T, FN>(w >> 12, sv[j], sx[j], tab);
                 }
 #endif
             }
@@ -601,19 +603,19 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
                 const uint32_t a = a_st + sizeof(T) * (w & 0xFFF);
                 if constexpr (FN == FN_IK) {
                     T ri, rk;
-                    eval_bin_ik<T>(w >> 12, lds_t<T>(a), lds_t<T>(a + sizeof(T) * TILE), ri, rk);
+                    eval_bin_ik<T>(w >> 12, lds_t<T>(a), lds_t<T>(a + sizeof(T) * TILE), ri, rk, tab);
                     sts_t<T>(a, ri);
                     sts_t<T>(a + sizeof(T) * TILE, rk);
                 } else {
-                    sts_t<T>(a, eval_bin<T, FN>(w >> 12, lds_t<T>(a), lds_t<T>(a + sizeof(T) * TILE)));
+                    sts_t<T>(a, eval_bin<T, FN>(w >> 12, lds_t<T>(a), lds_t<T>(a + sizeof(T) * TILE), tab));
                 }
 #else
                 const int w = homo ? (p | hw) : s_idx[p];
                 const int j = w & 0xFFF;
                 if constexpr (FN == FN_IK) {
-                    eval_bin_ik<T>(w >> 12, sv[j], sx[j], s_res[0][j], s_res[NOUT - 1][j]);
+                    eval_bin_ik<T>(w >> 12, sv[j], sx[j], s_res[0][j], s_res[NOUT - 1][j], tab);
                 } else {
-                    s_res[0][j] = eval_bin<T, FN>(w >> 12, sv[j], sx[j]);
+                    s_res[0][j] = eval_bin<T, FN>(w >> 12, sv[j], sx[j], tab);
                 }
 #endif
             }
@@ -625,9 +627,9 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
                     const int w = homo ? (p | hw) : s_idx[p];
                     const int j = w & 0xFFF;
                     if constexpr (FN == FN_IK) {
-                        eval_bin_ik<T>(w >> 12, sv[j], sx[j], s_res[0][j], s_res[NOUT - 1][j]);
+                        eval_bin_ik<T>(w >> 12, sv[j], sx[j], s_res[0][j], s_res[NOUT - 1][j], tab);
                     } else {
-                        s_res[0][j] = eval_bin<T, FN>(w >> 12, sv[j], sx[j]);
+                        s_res[0][j] = eval_bin<T, FN>(w >> 12, sv[j], sx[j], tab);
                     }
                 }
             }
@@ -748,6 +750,7 @@ __global__ void __launch_bounds__(wsk::NTHR, 1)
         fence_mbar_init();
     }
     fm_tables_init();   // log table to shared memory; ends with __syncthreads (covers the inits above)
+    const uint32_t tab = logtab_addr();
     auto tile_of = [&](int64_t k) { return int64_t(blockIdx.x) + k * int64_t(gridDim.x); };
     auto rem_of = [&](int64_t t) { return int(n - t * WTILE < WTILE ? n - t * WTILE : WTILE); };
     auto par = [](int64_t k) { return uint32_t((k / NST) & 1); };
@@ -865,9 +868,9 @@ __global__ void __launch_bounds__(wsk::NTHR, 1)
                 const int w = s_idx[st][p];
                 const int j = w & 0xFFF;
                 if constexpr (FN == FN_IK) {
-                    eval_bin_ik<T>(w >> 12, sv[j], sx[j], sv[j], sx[j]);
+                    eval_bin_ik<T>(w >> 12, sv[j], sx[j], sv[j], sx[j], tab);
                 } else {
-                    sv[j] = eval_bin<T, FN>(w >> 12, sv[j], sx[j]);
+                    sv[j] = eval_bin<T, FN>(w >> 12, sv[j], sx[j], tab);
                 }
             }
         }
@@ -909,16 +912,17 @@ __global__ void __launch_bounds__(256, 4)
     bessel_direct_kernel(const T *__restrict__ vin, const T *__restrict__ xin, T *__restrict__ out,
                          T *__restrict__ out2, int64_t n) {
     fm_tables_init();
+    const uint32_t tab = logtab_addr();
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
         const T v = __ldcs(vin + i), x = __ldcs(xin + i);
         const int b = bin_of<T, FN>(v, x);
         if constexpr (FN == FN_IK) {
             T ri, rk;
-            eval_bin_ik<T>(b, v, x, ri, rk);
+            eval_bin_ik<T>(b, v, x, ri, rk, tab);
             __stcs(out + i, ri);
             __stcs(out2 + i, rk);
         } else {
-            __stcs(out + i, eval_bin<T, FN>(b, v, x));
+            __stcs(out + i, eval_bin<T, FN>(b, v, x, tab));
         }
     }
 }

@@ -218,12 +218,12 @@ mu1_done:
 
 // log I = x - 1/2 log(2 pi x) + log S = x + 1/2 log(S^2 / (2 pi x))  (one log)
 template <typename T, bool IS_K, bool SAFE>
-__device__ __forceinline__ T log_bessel_mu(T v, T x) {
+__device__ __forceinline__ T log_bessel_mu(T v, T x, uint32_t tab = logtab_addr()) {
     if (!SAFE || x < Big<T>::v) {
         const T rx = fm_rcp(x);
         const T S = mu_series<T, IS_K>(v, rx);
         const T c = IS_K ? hc<T>(HC_PIO2) : hc<T>(HC_INV2PI);
-        return (IS_K ? -x : x) + T(0.5) * fm_log(S * S * rx * c);
+        return (IS_K ? -x : x) + T(0.5) * fm_log(S * S * rx * c, tab);
     }
     const T S = mu_series<T, IS_K>(v, T(1) / x);
     const T l2 = IS_K ? T(-0.22579135264472743) : T(1.8378770664093453);   // log(2/pi), log(2 pi)
@@ -340,7 +340,7 @@ template <> struct EtaC<float> {
 
 // vs, xs, rhos: v, x, rho scaled by the same power of two s; returns v*eta.
 template <typename T, bool SAFE>
-__device__ __forceinline__ T v_times_eta(T v, T x, T vs, T xs, T rhos, T rho) {
+__device__ __forceinline__ T v_times_eta(T v, T x, T vs, T xs, T rhos, T rho, uint32_t tab = logtab_addr()) {
     // band test on z = x/v without a division: |x - z0 v| < 0.03 v
     if (fabs(fma(-hc<T>(HC_ETA_HI), v, x)) < hc<T>(HC_ETA_BAND) * v) {
         const T rv = T(1) / v;
@@ -360,7 +360,7 @@ __device__ __forceinline__ T v_times_eta(T v, T x, T vs, T xs, T rhos, T rho) {
         return fma(v, lq, rho);
     }
     const T q = xs * fm_rcp(vs + rhos);
-    return fma(v, fm_log_acc(q), rho);
+    return fma(v, fm_log_acc(q, tab), rho);
 }
 
 // Number of U_K terms.  The paper's Table 1 fits regions for U4/U6/U9/U13 and
@@ -375,7 +375,7 @@ __device__ __forceinline__ T v_times_eta(T v, T x, T vs, T xs, T rhos, T rho) {
 // allows.  The bins (select_eval_hw) use K = KU_A/KU_B/KU_C/13.
 
 template <typename T, bool IS_K, int KU, bool SAFE>
-__device__ __forceinline__ T log_bessel_u(T v, T x) {
+__device__ __forceinline__ T log_bessel_u(T v, T x, uint32_t tab = logtab_addr()) {
     // rescale by s = 2^-e, e = the binary exponent of max(v, x), where v^2 + x^2 could
     // overflow (wide-range guard): then max(vs, xs) is in [1, 2)
     const bool big = SAFE && fmax(v, x) >= Big<T>::v;
@@ -394,10 +394,10 @@ __device__ __forceinline__ T log_bessel_u(T v, T x) {
 #pragma unroll
     for (int k = KU - 1; k >= 1; --k) acc = fma(acc, w, uk_row<T>(k, t2));
     const T d = acc * w;                         // S - 1
-    const T veta = v_times_eta<T, SAFE>(v, x, vs, xs, rhos, rho);
+    const T veta = v_times_eta<T, SAFE>(v, x, vs, xs, rhos, rho, tab);
     // log S + 1/2 log(y_true c) with y_true = s y
     const T c = IS_K ? hc<T>(HC_PIO2) : hc<T>(HC_INV2PI);
-    const T tail = log1p_small<T, L1PDeg<T, KU>::v>(d) + T(0.5) * (fm_log(y * c) + ls);
+    const T tail = log1p_small<T, L1PDeg<T, KU>::v>(d) + T(0.5) * (fm_log(y * c, tab) + ls);
     return IS_K ? tail - veta : veta + tail;
 }
 
@@ -409,7 +409,7 @@ __device__ __forceinline__ T log_bessel_u(T v, T x) {
 // by (-1)^k.  One rsqrt, one Horner pass per P_k, one v*eta (its log) serve
 // both results; only the final log per function is separate.
 template <typename T, int KU>
-__device__ __forceinline__ void log_bessel_u_ik(T v, T x, T &li, T &lk) {
+__device__ __forceinline__ void log_bessel_u_ik(T v, T x, T &li, T &lk, uint32_t tab = logtab_addr()) {
     const T rho2 = fma(v, v, x * x);
     const T y = fm_rsqrt(rho2);                  // 1 / rho = t / v
     const T rho = rho2 * y;
@@ -425,17 +425,17 @@ __device__ __forceinline__ void log_bessel_u_ik(T v, T x, T &li, T &lk) {
 #pragma unroll
     for (int k = KO - 2; k >= 1; k -= 2) o = fma(o, w2, uk_row<T>(k, t2));
     o *= y;
-    const T veta = v_times_eta<T, false>(v, x, v, x, rho, rho);
+    const T veta = v_times_eta<T, false>(v, x, v, x, rho, rho, tab);
     // log S_I = log1p(e + o), log S_K = log1p(e - o); one log of y for both:
     // 1/2 log(y pi/2) = 1/2 log(y/(2 pi)) + log(pi)
-    const T hl = T(0.5) * fm_log(y * hc<T>(HC_INV2PI));
+    const T hl = T(0.5) * fm_log(y * hc<T>(HC_INV2PI), tab);
     li = veta + (hl + log1p_small<T, L1PDeg<T, KU>::v>(e + o));
     lk = (hl + hc<T>(HC_LNPI)) + log1p_small<T, L1PDeg<T, KU>::v>(e - o) - veta;
 }
 
 
 template <typename T>
-__device__ __forceinline__ void log_bessel_mu_ik(T v, T x, T &li, T &lk) {
+__device__ __forceinline__ void log_bessel_mu_ik(T v, T x, T &li, T &lk, uint32_t tab = logtab_addr()) {
 #if B200_MUFACT
     // Carry T_k = k! term_k: T_k = T_{k-1} (c mu - c (2k-1)^2) (one FMA with an immediate
     // square, one multiply) and accumulate S_I, S_K with the constants (-1)^k / k!, 1/k!
@@ -481,8 +481,8 @@ mu_done:
     sk = ev + od;
 #endif
     const T SI = fabs(si), SK = fabs(sk);
-    li = x + T(0.5) * fm_log(SI * SI * rx * hc<T>(HC_INV2PI));
-    lk = -x + T(0.5) * fm_log(SK * SK * rx * hc<T>(HC_PIO2));
+    li = x + T(0.5) * fm_log(SI * SI * rx * hc<T>(HC_INV2PI), tab);
+    lk = -x + T(0.5) * fm_log(SK * SK * rx * hc<T>(HC_PIO2), tab);
 #elif B200_MUEO
     // The two series differ only by (-1)^k: with E = 1 + sum of the even terms and
     // O = sum of the odd ones, S_K = E + O and S_I = E - O, so every term is added
@@ -506,8 +506,8 @@ mu_done:
         if (k >= 3 && fabs(term) <= Tr<T>::eps * T(0.25) * fabs(E - O)) break;
     }
     const T SI = fabs(E - O), SK = fabs(E + O);
-    li = x + T(0.5) * fm_log(SI * SI * rx * hc<T>(HC_INV2PI));
-    lk = -x + T(0.5) * fm_log(SK * SK * rx * hc<T>(HC_PIO2));
+    li = x + T(0.5) * fm_log(SI * SI * rx * hc<T>(HC_INV2PI), tab);
+    lk = -x + T(0.5) * fm_log(SK * SK * rx * hc<T>(HC_PIO2), tab);
 #else
     const T rx = fm_rcp(x);
     const T mu = T(4) * v * v;
@@ -546,8 +546,8 @@ mu_done:
         if (k >= 3 && fabs(term) <= Tr<T>::eps * T(0.25) * fabs(si)) break;
     }
     const T SI = fabs(si), SK = fabs(sk);
-    li = x + T(0.5) * fm_log(SI * SI * rx * hc<T>(HC_INV2PI));
-    lk = -x + T(0.5) * fm_log(SK * SK * rx * hc<T>(HC_PIO2));
+    li = x + T(0.5) * fm_log(SI * SI * rx * hc<T>(HC_INV2PI), tab);
+    lk = -x + T(0.5) * fm_log(SK * SK * rx * hc<T>(HC_PIO2), tab);
 #endif
 }
 
@@ -571,7 +571,7 @@ mu_done:
 // b_k <= eps * sum reads Q_k <= eps * N_k.  In the fallback region (x <= 30,
 // v <= 12.7, at most ~45 terms) P_K < 1e130 and N_K < 1e150: no rescaling.
 template <typename T, bool SAFE>
-__device__ __forceinline__ T log_iv_series(T v, T x) {
+__device__ __forceinline__ T log_iv_series(T v, T x, uint32_t tab = logtab_addr()) {
     if (x == T(0)) return v == T(0) ? T(0) : T(-CUDART_INF);
     if constexpr (sizeof(T) == 8) {
         const T q = T(0.25) * x * x;
@@ -600,11 +600,11 @@ __device__ __forceinline__ T log_iv_series(T v, T x) {
 #pragma unroll
         for (int j = B200_RGAMMA_NT - 2; j >= 1; --j) g = fma(g, mu, T(c_rg_d[j]));
         const T gm1 = g * mu;
-        const T lx = SAFE ? fm_log_wide(x) - T(0.6931471805599453) : fm_log(T(0.5) * x);   // log(x/2)
+        const T lx = SAFE ? fm_log_wide(x) - T(0.6931471805599453) : fm_log(T(0.5) * x, tab);   // log(x/2)
         if (nl == 0) {
             // v < 1/2: log I = v log(x/2) + log1p(gm1) + log1p(M/P) -- every term with
             // relative accuracy (|log I| < 1 here for small v and x: DESIGN.md R1)
-            return fma(v, lx, fm_log1p(gm1) + fm_log1p(fm_div(M, P)));
+            return fma(v, lx, fm_log1p(gm1, tab) + fm_log1p(fm_div(M, P), tab));
         }
         T pr = T(1), m = mu;
         for (int j = 1; j < nl; j += 2) {      // factor pairs (mu+j)(mu+j+1)
@@ -613,7 +613,7 @@ __device__ __forceinline__ T log_iv_series(T v, T x) {
             pr *= a * m;
         }
         if (nl & 1) pr *= m + T(1);
-        return fma(v, lx, fm_log(fm_div((M + P) * (T(1) + gm1), P * pr)));
+        return fma(v, lx, fm_log(fm_div((M + P) * (T(1) + gm1), P * pr), tab));
     }
     const T q = T(0.25) * x * x;
     T b = T(1), S = T(1);
@@ -696,9 +696,9 @@ __device__ __forceinline__ void sinhc_cosh(T e, T E, T &shc, T &ch) {
 // SAFE = true (the slow bin): any x > 0 including subnormals -- ln(2/x) = ln 2 -
 // log x by the library log (0.5 x would underflow), |mu ln(2/x)| <= 372.5.
 template <typename T, bool SAFE = false>
-__device__ __forceinline__ T temme_kmu(T mu, T x, T &sum, T &sum1) {
+__device__ __forceinline__ T temme_kmu(T mu, T x, T &sum, T &sum1, uint32_t tab = logtab_addr()) {
     const T eps = Tr<T>::eps;
-    const T d = SAFE ? T(0.6931471805599453) - log(x) : -fm_log(T(0.5) * x);   // ln(2/x)
+    const T d = SAFE ? T(0.6931471805599453) - log(x) : -fm_log(T(0.5) * x, tab);   // ln(2/x)
     const T e = mu * d;
     // pi mu / sin(pi mu) = 1 / sum_k SINPI[k] mu^(2k)  (|mu| <= 1/2, tables.h)
     const T m2 = mu * mu;
@@ -736,7 +736,7 @@ __device__ __forceinline__ T temme_kmu(T mu, T x, T &sum, T &sum1) {
         }
         if (fabs(del) < fabs(sum) * eps) break;
     }
-    return SAFE ? log(sum) : fm_log(sum);
+    return SAFE ? log(sum) : fm_log(sum, tab);
 }
 
 // K_mu(x) and K_{mu+1}(x), |mu| <= 1/2, on the band 2 < x <= 30 of the
@@ -776,7 +776,7 @@ __device__ __forceinline__ T two_cosh_small(T z) {
 // kl (optional): K_mu e^x = (h/2) A, so log K_mu = -x + log kl (callers that
 // fold further factors into one log use it).
 template <typename T>
-__device__ __forceinline__ T trap_kmu(T mu, T x, T &rho, T *kl = nullptr) {
+__device__ __forceinline__ T trap_kmu(T mu, T x, T &rho, uint32_t tab = logtab_addr(), T *kl = nullptr) {
     // f64: h = pi^2 / (42 + 0.8 x) (measured largest admissible step for 2^-53, R14);
     // f32: the error ~ exp(-pi^2 / h) only has to reach ~2^-26: h = pi^2 / (24 + 0.45 x)
     const T h = hc<T>(HC_PI2) * fm_rcp(sizeof(T) == 8 ? fma(T(0.8), x, T(42)) : fma(T(0.45), x, T(24)));
@@ -829,18 +829,18 @@ __device__ __forceinline__ T trap_kmu(T mu, T x, T &rho, T *kl = nullptr) {
         *kl = T(0.5) * h * A;
         return T(0);   // unused by such callers
     }
-    return -x + fm_log(T(0.5) * h * A);
+    return -x + fm_log(T(0.5) * h * A, tab);
 }
 
 template <typename T, bool SAFE>
-__device__ __forceinline__ T log_kv_fallback(T v, T x) {
+__device__ __forceinline__ T log_kv_fallback(T v, T x, uint32_t tab = logtab_addr()) {
     const int nl = int(floor(v + T(0.5)));
     const T mu = v - T(nl);
     // forward recurrence K_{nu+1} = K_{nu-1} + (2 nu / x) K_nu (stable for K)
     // on the ratios K_{mu+i} / K_mu, from i = 0, 1 up to i = nl
     if (x > T(2)) {
         T rho;
-        const T lk = trap_kmu<T>(mu, x, rho);
+        const T lk = trap_kmu<T>(mu, x, rho, tab);
         const T tox = T(2) * fm_rcp(x);
         // x > 2, v <= 12.7: K_v / K_mu < 1e12, no rescaling needed.  The coefficient
         // 2 nu / x advances by one addition of 2/x per step (< 13 roundings)
@@ -852,10 +852,10 @@ __device__ __forceinline__ T log_kv_fallback(T v, T x) {
             km = kp;
             kp = kn;
         }
-        return nl == 0 ? lk : lk + fm_log(kp);
+        return nl == 0 ? lk : lk + fm_log(kp, tab);
     }
     T S, S1;
-    const T lk = temme_kmu<T, SAFE>(mu, x, S, S1);
+    const T lk = temme_kmu<T, SAFE>(mu, x, S, S1, tab);
     if (nl == 0) return lk;
     if (x >= T(1e-6)) {
         // (2 * 13 / 1e-6)^13 < 1e97: the unscaled ratio stays in the double range
@@ -869,7 +869,7 @@ __device__ __forceinline__ T log_kv_fallback(T v, T x) {
             km = kp;
             kp = kn;
         }
-        return lk + T(fm_log(kp));
+        return lk + T(fm_log(kp, tab));
     }
     // x < 1e-6 (any x > 0, subnormals included): scaled ratios.  With s = x/2 and
     // a = 2 max(-mu, 0), k_i = (K_{mu+i}/K_mu) s^(i-a) (i >= 1) is O(1) for every i
@@ -877,10 +877,10 @@ __device__ __forceinline__ T log_kv_fallback(T v, T x) {
     // nothing overflows or underflows even at x = 5e-324:
     //   k_1 = (S1/S) s^-a,  k_2 = s^(2-a) + (mu+1) k_1,  k_{i+1} = s^2 k_{i-1} + (mu+i) k_i,
     //   log K_v = log K_mu + log k_nl - (nl - a) log s.
-    const double ls = (SAFE ? fm_log_wide(double(x)) : fm_log(double(x))) - 0.6931471805599453;   // log(x/2)
+    const double ls = (SAFE ? fm_log_wide(double(x)) : fm_log(double(x), tab)) - 0.6931471805599453;   // log(x/2)
     const double a = mu < T(0) ? -2.0 * double(mu) : 0.0;
-    const double k1 = mu < T(0) ? fm_exp(fm_log(double(S1)) - fm_log(double(S)) - a * ls) : double(S1) / double(S);
-    if (nl == 1) return lk + T(fm_log(k1) - (1.0 - a) * ls);
+    const double k1 = mu < T(0) ? fm_exp(fm_log(double(S1), tab) - fm_log(double(S), tab) - a * ls) : double(S1) / double(S);
+    if (nl == 1) return lk + T(fm_log(k1, tab) - (1.0 - a) * ls);
     const double s2 = 0.25 * double(x) * double(x);   // underflows harmlessly for tiny x
     double km = k1, kp = fm_exp((2.0 - a) * ls) + double(mu + T(1)) * k1, nu = double(mu) + 1.0;
     for (int i = 2; i < nl; ++i) {
@@ -889,7 +889,7 @@ __device__ __forceinline__ T log_kv_fallback(T v, T x) {
         km = kp;
         kp = kn;
     }
-    return lk + T(fm_log(kp) - (double(nl) - a) * ls);
+    return lk + T(fm_log(kp, tab) - (double(nl) - a) * ls);
 }
 
 // Fused fallback for 2 < x <= 30, v <= 12.7 (FN_IK): log K_v as in
@@ -908,7 +908,7 @@ __device__ __forceinline__ T log_kv_fallback(T v, T x) {
 // series (f64 only: there |y| < 4.1e98 and K_{v+1}/K_mu < 1e97, so neither
 // the recurrences nor x (K_{v+1} + r K_v) / K_mu leave the double range).
 template <typename T, bool TEMME = false>
-__device__ __forceinline__ void log_ivkv_trap(T v, T x, T &ri, T &rk) {
+__device__ __forceinline__ void log_ivkv_trap(T v, T x, T &ri, T &rk, uint32_t tab = logtab_addr()) {
     const int nl = int(floor(v + T(0.5)));
     const T mu = v - T(nl);
     const T tox = T(2) * fm_rcp(x);
@@ -918,10 +918,10 @@ __device__ __forceinline__ void log_ivkv_trap(T v, T x, T &ri, T &rk) {
     T kl;
     if constexpr (TEMME) {
         T S1;
-        (void)temme_kmu<T>(mu, x, kl, S1);
+        (void)temme_kmu<T>(mu, x, kl, S1, tab);
         rho = T(2) * S1 * fm_rcp(x * kl);
     } else {
-        (void)trap_kmu<T>(mu, x, rho, &kl);
+        (void)trap_kmu<T>(mu, x, rho, tab, &kl);
     }
     // kp = K_v / K_mu, kn = K_{v+1} / K_mu (one recurrence step past v); the
     // coefficient 2 nu / x advances by one addition of 2/x per step
@@ -957,12 +957,12 @@ __device__ __forceinline__ void log_ivkv_trap(T v, T x, T &ri, T &rk) {
     }
     // y0 = y_v, y1 = y_{v+1}: r = y1 / y0;  1 / (I_v K_mu) = x (K_{v+1} + r K_v) / K_mu
     const T off = TEMME ? T(0) : -x;
-    rk = off + fm_log(kl * km);
+    rk = off + fm_log(kl * km, tab);
     if constexpr (sizeof(T) == 8) {
-        ri = -off - fm_log(kl * x * fma(km, y1, kp * y0) * fm_rcp(y0));
+        ri = -off - fm_log(kl * x * fma(km, y1, kp * y0) * fm_rcp(y0), tab);
     } else {
         // f32: kp y0 can pass FLT_MAX near x = 0.1 (~1e27 * 1e17); take the ratio first
-        ri = -off - fm_log(kl * x * fma(km, y1 * fm_rcp(y0), kp));
+        ri = -off - fm_log(kl * x * fma(km, y1 * fm_rcp(y0), kp), tab);
     }
 }
 

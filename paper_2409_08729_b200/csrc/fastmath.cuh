@@ -120,15 +120,26 @@ __device__ __forceinline__ void fm_tables_init() {
 __device__ __forceinline__ void fm_tables_init() {}
 #endif
 
-// log(a) for finite normal a > 0.
-__device__ __forceinline__ double fm_log(double a) {
+#if B200_SMEM_LOG
+// 32-bit shared address of the log table.  The kernels compute it once and pass it down
+// (fm_log(a, tab)): on sm_100a a shared address carries the CTA's cluster rank, and ptxas
+// re-derives it (S2UR SR_CgaCtaId + three uniform operations) at every table access
+// otherwise.
+__device__ __forceinline__ uint32_t logtab_addr() { return uint32_t(__cvta_generic_to_shared(s_logtab)); }
+#else
+__device__ __forceinline__ uint32_t logtab_addr() { return 0u; }
+#endif
+
+// log(a) for finite normal a > 0; tab = logtab_addr() (computed by the caller).
+__device__ __forceinline__ double fm_log(double a, uint32_t tab) {
     const int hi = __double2hiint(a), lo = __double2loint(a);
     const int t = hi - B200_LOG_HI_OFF;
     const int e = t >> 20;                                   // a = 2^e * m, m in [sqrt(1/2), sqrt(2))
     const int i = (t >> (20 - B200_LOG_TAB_BITS)) & ((1 << B200_LOG_TAB_BITS) - 1);
     const double m = __hiloint2double(hi - (e << 20), lo);
 #if B200_SMEM_LOG
-    const double2 c = s_logtab[i];
+    double2 c;   // the table is written once at kernel start (fm_tables_init, then a barrier)
+    asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(c.x), "=d"(c.y) : "r"(tab + 16u * uint32_t(i)));
     const double tlo = 0.0;
 #else
     const double2 c = __ldg(reinterpret_cast<const double2 *>(&g_logtab[i]));
@@ -154,6 +165,7 @@ __device__ __forceinline__ double fm_log(double a) {
 #endif
     return h + (r + fma(r * r, p, l));
 }
+__device__ __forceinline__ double fm_log(double a) { return fm_log(a, logtab_addr()); }
 
 // exp(y) from yp = y * 64/ln2, already scaled by the caller (who folds the factor into a
 // product it forms anyway), -65000 <= yp <= 0: the reduction is yp - round(yp), exact,
@@ -221,12 +233,14 @@ __device__ __forceinline__ double fm_rsqrt(double a) {
 
 // log(1 + d) for d > -1 with relative accuracy when |d| is small: u = 1 + d rounds,
 // the first-order correction restores the lost low part of d (u - 1 is exact).
-__device__ __forceinline__ double fm_log1p(double d) {
+__device__ __forceinline__ double fm_log1p(double d, uint32_t tab) {
     const double u = 1.0 + d;
     if (u == 1.0) return d;
-    return fm_log(u) - ((u - 1.0) - d) * fm_rcp(u);
+    return fm_log(u, tab) - ((u - 1.0) - d) * fm_rcp(u);
 }
+__device__ __forceinline__ double fm_log1p(double d) { return fm_log1p(d, logtab_addr()); }
 
+__device__ __forceinline__ double fm_log_acc(double a, uint32_t tab) { return fm_log(a, tab); }
 __device__ __forceinline__ double fm_log_acc(double a) { return fm_log(a); }
 
 // log(a) for any finite a > 0 (subnormals through the library function).
@@ -244,8 +258,10 @@ __device__ __forceinline__ float fm_log_wide(float a) { return logf(a); }
 // log whose absolute error is multiplied by a large factor (v log(x/(v+rho)) in the U
 // expansion, where v eta cancels towards its root): the accurate library logf in f32
 __device__ __forceinline__ float fm_log_acc(float a) { return logf(a); }
+__device__ __forceinline__ float fm_log_acc(float a, uint32_t) { return logf(a); }
 #if B200_F32FAST
 __device__ __forceinline__ float fm_log(float a) { return __logf(a); }
+__device__ __forceinline__ float fm_log(float a, uint32_t) { return __logf(a); }
 __device__ __forceinline__ float fm_exp(float y) { return __expf(fmaxf(y, -87.0f)); }
 __device__ __forceinline__ float fm_exp_nc(float y) { return __expf(y); }
 __device__ __forceinline__ float fm_rcp(float a) {
@@ -261,6 +277,7 @@ __device__ __forceinline__ float fm_rsqrt(float a) {
 }
 #else
 __device__ __forceinline__ float fm_log(float a) { return logf(a); }
+__device__ __forceinline__ float fm_log(float a, uint32_t) { return logf(a); }
 __device__ __forceinline__ float fm_exp(float y) { return expf(y); }
 __device__ __forceinline__ float fm_exp_nc(float y) { return expf(y); }
 __device__ __forceinline__ float fm_rcp(float a) { return __frcp_rn(a); }
