@@ -343,7 +343,9 @@ template <typename T, bool SAFE>
 __device__ __forceinline__ T v_times_eta(T v, T x, T vs, T xs, T rhos, T rho, uint32_t tab = logtab_addr()) {
     // band test on z = x/v without a division: |x - z0 v| < 0.03 v
     if (fabs(fma(-hc<T>(HC_ETA_HI), v, x)) < hc<T>(HC_ETA_BAND) * v) {
-        const T rv = T(1) / v;
+        // 1/v by the MUFU-seeded reciprocal (<= 2 ulp): its error enters z = x/v but not
+        // z + zlo, whose residual x - z v is exact by FMA (z + zlo = x/v to ~2^-100)
+        const T rv = SAFE ? T(1) / v : fm_rcp(v);
         const T z = x * rv;
         const T zlo = fma(-z, v, x) * rv;
         const T d = (z - EtaC<T>::hi) + (zlo - EtaC<T>::lo);
