@@ -139,6 +139,9 @@ constexpr int KMU = 26;
 #ifndef B200_MUEO
 #define B200_MUEO 0
 #endif
+#ifndef B200_TEMME_UNROLL
+#define B200_TEMME_UNROLL 1   // 1: Temme's series, terms 1..20 written out (0: rolled loop)
+#endif
 #ifndef B200_MUF
 #define B200_MUF 1
 #endif
@@ -720,24 +723,56 @@ __device__ __forceinline__ T temme_kmu(T mu, T x, T &sum, T &sum1, uint32_t tab 
     T c = T(1);
     const T dd = T(0.25) * x * x;
     sum1 = p;
-    T fi = T(0);
-    for (int i = 1; i < 100; i += 2) {          // two terms per stop test
-        T del;
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            fi += T(1);
-            // 1/(i-mu), 1/(i+mu) and 1/(i^2-mu^2) share one reciprocal
-            const T inv = fm_rcp(fma(fi, fi, -m2));
-            ff = (fi * ff + p + q) * inv;
-            c *= dd * c_inv_k<T>(i + u);
-            p *= (fi + mu) * inv;
-            q *= (fi - mu) * inv;
-            del = c * ff;
-            sum += del;
-            sum1 += c * (p - fi * ff);
-        }
-        if (fabs(del) < fabs(sum) * eps) break;
+    T del;
+#if B200_TEMME_UNROLL
+    // terms 1..20 written out (x <= 2 needs at most ~19: c_k <= 1/k!), so k, k^2 and 1/k are
+    // immediates / uniform constants instead of a floating counter and an indexed load
+#define B200_TM_T(k)                                                         \
+    {                                                                        \
+        const T inv = fm_rcp(T(double((k) * (k))) - m2);                     \
+        ff = (T(double(k)) * ff + p + q) * inv;                              \
+        c *= dd * c_inv_k<T>(k);                                             \
+        p *= (T(double(k)) + mu) * inv;                                      \
+        q *= (T(double(k)) - mu) * inv;                                      \
+        del = c * ff;                                                        \
+        sum += del;                                                          \
+        sum1 += c * (p - T(double(k)) * ff);                                 \
     }
+#define B200_TM_STOP if (fabs(del) < fabs(sum) * eps) goto temme_done;
+    B200_TM_T(1) B200_TM_T(2) B200_TM_STOP B200_TM_T(3) B200_TM_T(4) B200_TM_STOP
+    B200_TM_T(5) B200_TM_T(6) B200_TM_STOP B200_TM_T(7) B200_TM_T(8) B200_TM_STOP
+    B200_TM_T(9) B200_TM_T(10) B200_TM_STOP B200_TM_T(11) B200_TM_T(12) B200_TM_STOP
+    B200_TM_T(13) B200_TM_T(14) B200_TM_STOP B200_TM_T(15) B200_TM_T(16) B200_TM_STOP
+    B200_TM_T(17) B200_TM_T(18) B200_TM_STOP B200_TM_T(19) B200_TM_T(20) B200_TM_STOP
+#undef B200_TM_T
+#undef B200_TM_STOP
+    {
+        T fi = T(20);
+        for (int i = 21; i < 100; i += 2) {      // not reached for x <= 2
+#else
+    {
+        T fi = T(0);
+        for (int i = 1; i < 100; i += 2) {      // two terms per stop test
+#endif
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                fi += T(1);
+                // 1/(i-mu), 1/(i+mu) and 1/(i^2-mu^2) share one reciprocal
+                const T inv = fm_rcp(fma(fi, fi, -m2));
+                ff = (fi * ff + p + q) * inv;
+                c *= dd * c_inv_k<T>(i + u);
+                p *= (fi + mu) * inv;
+                q *= (fi - mu) * inv;
+                del = c * ff;
+                sum += del;
+                sum1 += c * (p - fi * ff);
+            }
+            if (fabs(del) < fabs(sum) * eps) break;
+        }
+    }
+#if B200_TEMME_UNROLL
+temme_done:
+#endif
     return SAFE ? log(sum) : fm_log(sum, tab);
 }
 
