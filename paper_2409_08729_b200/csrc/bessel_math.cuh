@@ -139,6 +139,9 @@ constexpr int KMU = 26;
 #ifndef B200_MUEO
 #define B200_MUEO 0
 #endif
+#ifndef B200_SERIES_UNROLL
+#define B200_SERIES_UNROLL 1  // 1: the f64 power series of log I, terms 1..48 written out (0: rolled)
+#endif
 #ifndef B200_TEMME_UNROLL
 #define B200_TEMME_UNROLL 1   // 1: Temme's series, terms 1..20 written out (0: rolled loop)
 #endif
@@ -583,7 +586,29 @@ __device__ __forceinline__ T log_iv_series(T v, T x, uint32_t tab = logtab_addr(
         // M_k = N_k - P_k = P_k sum_{1<=j<=k} b_j (carried instead of N: the sum minus its
         // leading 1 keeps full relative accuracy when the sum is ~1, e.g. log I_0(x) ~ x^2/4)
         T M = T(0), P = T(1), Q = T(1), vk = v, kd = T(0);
+#if B200_SERIES_UNROLL
+        // terms 1..48 written out (x <= 30, the series region, needs at most ~45): D_k =
+        // k (v + k) is one FMA with immediates k, k^2 instead of two counter additions and
+        // a product (and one rounding instead of two)
+#define B200_SR_T(k)                                                         \
+        {                                                                    \
+            const T d = fma(T(double(k)), v, T(double((k) * (k))));          \
+            Q *= q;                                                          \
+            M = fma(M, d, Q);                                                \
+            P *= d;                                                          \
+        }
+#define B200_SR_4(k) B200_SR_T(k) B200_SR_T((k) + 1) B200_SR_T((k) + 2) B200_SR_T((k) + 3) \
+        if (Q <= (M + P) * Tr<T>::eps) goto series_done;
+        B200_SR_4(1) B200_SR_4(5) B200_SR_4(9) B200_SR_4(13) B200_SR_4(17) B200_SR_4(21)
+        B200_SR_4(25) B200_SR_4(29) B200_SR_4(33) B200_SR_4(37) B200_SR_4(41) B200_SR_4(45)
+#undef B200_SR_T
+#undef B200_SR_4
+        vk = v + T(48);
+        kd = T(48);
+        for (int k = 49; k < 400; k += 4) {     // not reached for x <= 30
+#else
         for (int k = 1; k < 400; k += 4) {      // four terms per trip, one stop test
+#endif
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 vk += T(1);
@@ -595,6 +620,9 @@ __device__ __forceinline__ T log_iv_series(T v, T x, uint32_t tab = logtab_addr(
             }
             if (Q <= (M + P) * Tr<T>::eps) break;
         }
+#if B200_SERIES_UNROLL
+    series_done:
+#endif
         // a_0 = 1/Gamma(v+1) = rg(mu) / prod_{j=1..n} (mu + j), v = n + mu, |mu| <= 1/2,
         // rg(z) = 1/Gamma(1+z) by its Taylor series (tables.h) -- no lgamma call;
         // rg(mu) = 1 + gm1 with gm1 = mu (c_1 + mu (c_2 + ...)) (c_0 = 1)
