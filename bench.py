@@ -177,6 +177,18 @@ def cpu_baseline(target_s=12.0, seed=123):
                       f"v-major, 11 orders), binary128 oracle, OpenMP over {cores} threads, {done_t:.1f} s"}
 
 
+def bench_config(n_per_v, ws):
+    """The bench workload's `config` (shared by both arms: the reference arm times bounded
+    samples of this same workload, described in its cpu_baseline.sample)."""
+    n = N_ORDERS * n_per_v
+    return {"workload": f"log I_v and log K_v of every pair of v in {{2^0..2^10}} x {n_per_v} "
+                        f"x~U[1,100] per GPU ({n} pairs, v-major; configs[1]+configs[2]), "
+                        "one fused pass (b200_log_ivkv_f64)",
+            "pairs_per_gpu": n, "evals_per_step": 2 * n * ws,
+            "l2": "inputs_larger_than_l2 (3.5 GB in, 3.5 GB out per step)",
+            "parallelism": f"dp{ws} (contiguous batch per rank, no collective)"}
+
+
 def run_reference(args):
     ws, rank, _ = _env_int("WORLD_SIZE", 1), _env_int("RANK", 0), 0
     if rank != 0:
@@ -201,10 +213,11 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tt / len(ts),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f128",
             "data": "synthetic",
-            "config": {"workload": "bench grid sample: v in {2^0..2^10}, x ~ U[1,100]; "
-                                   f"{ev // len(ts)} evals per step (bounded sample)"},
+            "config": bench_config(args.n_per_v, ws),
             "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"{ev // len(ts)} evaluations per step, binary128, OpenMP x{cores}"},
+                             "sample": f"each step: {ev // len(ts)} evaluations (log I and log K) on pairs "
+                                       "drawn from this workload (bench grid, v-major, 11 orders), binary128, "
+                                       f"OpenMP x{cores}"},
             "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -485,12 +498,7 @@ def run_ours(args):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"log I_v and log K_v of every pair of v in {{2^0..2^10}} x {n_per_v} "
-                               f"x~U[1,100] per GPU ({n} pairs, v-major; configs[1]+configs[2]), "
-                               "one fused pass (b200_log_ivkv_f64)",
-                   "pairs_per_gpu": n, "evals_per_step": evals_per_step,
-                   "l2": "inputs_larger_than_l2 (3.5 GB in, 3.5 GB out per step)",
-                   "parallelism": f"dp{ws} (contiguous batch per rank, no collective)"},
+        "config": bench_config(n_per_v, ws),
         "roofline": roof,
         "gpu_launches": launches,
         "nonfinite_outputs": nonfinite,
