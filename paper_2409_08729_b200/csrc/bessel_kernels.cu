@@ -74,6 +74,9 @@ constexpr int BIN_SLOW = 7;           // out-of-range / special inputs (slow_eva
 #ifndef B200_SADDR2
 #define B200_SADDR2 1                 // 1: the same in the other kernels' evaluation loop
 #endif
+#ifndef B200_C4
+#define B200_C4 1                     // 1: 4-bit per-thread bin counters, widened once per thread (0: 64-bit shifts)
+#endif
 #ifndef B200_PLOOP
 #define B200_PLOOP 1                  // 1: the unpadded evaluation loop runs on the slot index (0: element counter)
 #endif
@@ -454,6 +457,23 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
         }
         const uint64_t c8 = (uint64_t(chi) << 32) | clo;
 #else
+#if B200_C4
+        // 4-bit per-thread counters (ITEMS <= 7 < 16 per key), one 32-bit shift and add per
+        // element; widened once per thread to the 8-bit fields of the warp scan: the even
+        // keys' nibbles go to bytes 0, 2, 4, 6 and the odd keys' to bytes 1, 3, 5, 7
+        uint32_t c4 = 0;
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const int j = tid + i * TPB;
+            lb[i] = -1;
+            if (j < rem) {
+                lb[i] = bin_of<T, FN>(sv[j], sx[j]);
+                c4 += 1u << (PADK ? 28 - 4 * lb[i] : 4 * lb[i]);     // PADK: sort key 7 - bin, costliest first
+            }
+        }
+        const uint32_t ev = c4 & 0x0F0F0F0Fu, od = (c4 >> 4) & 0x0F0F0F0Fu;
+        const uint64_t c8 = uint64_t(__byte_perm(ev, od, 0x5140)) | (uint64_t(__byte_perm(ev, od, 0x7362)) << 32);
+#else
         uint64_t c8 = 0;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
@@ -464,6 +484,7 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
                 c8 += 1ull << (PADK ? 56 - 8 * lb[i] : 8 * lb[i]);   // PADK: sort key 7 - bin, costliest first
             }
         }
+#endif
 #endif
         // 2. warp-inclusive scan of the packed counts, per-warp totals to smem
         uint64_t incl = c8;
