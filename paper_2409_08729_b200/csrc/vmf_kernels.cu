@@ -117,37 +117,40 @@ __global__ void __launch_bounds__(CS_TPB) colsum_partial_kernel(const T *__restr
     }
 }
 
-// Stage 2: colsum[j] (+)= sum_s part[s*d + j] in a fixed order: warp w of a
-// CTA sums slabs w, w + 8, w + 16, ... of 32 consecutive columns (one 256-byte
-// row segment per load) into four interleaved accumulators (four independent
-// loads in flight per warp instead of one dependent chain), combined in a fixed
-// order, then the 8 warp partials are added in warp order -- deterministic for a
-// given slab count.  d/32 CTAs.  Block 0 also writes the row-count slot
-// colsum[d] (+)= n when with_count (no separate launch).
-constexpr int CR_WARPS = 8;
+// Stage 2: colsum[j] (+)= sum_s part[s*d + j] in a fixed order: warp w of an
+// NW-warp CTA sums slabs w, w + NW, w + 2 NW, ... of 32 consecutive columns (one
+// 256-byte row segment per load), eight slabs per pass loaded together (predicated,
+// independent: one memory round trip per pass instead of a dependent chain) and added
+// in a fixed tree; the NW warp partials are then added in warp order -- deterministic
+// for a given slab count.  d/32 CTAs of 32 warps when there are more than 64 slabs
+// (d = 2048: 222 slabs, 13 -> 3 us against 8 warps with dependent chains), else 8.
+// Block 0 also writes the row-count slot colsum[d] (+)= n when with_count (no
+// separate launch).
+template <int CR_WARPS>
 __global__ void __launch_bounds__(32 * CR_WARPS) colsum_reduce_kernel(const double *__restrict__ part, int64_t nslab,
                                                                      int64_t d, double *__restrict__ colsum,
                                                                      int accumulate, int with_count, double n_rows) {
-    __shared__ double sh[CR_WARPS][32];
+    __shared__ double sh[CR_WARPS][33];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     pdl_wait();                // the partials of the preceding grid are complete and visible
     pdl_launch_dependents();
     if (with_count && blockIdx.x == 0 && threadIdx.x == 0) colsum[d] = accumulate ? colsum[d] + n_rows : n_rows;
     for (int64_t c0 = int64_t(blockIdx.x) * 32; c0 < d; c0 += int64_t(gridDim.x) * 32) {
         const int64_t j = c0 + lane;
-        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        double s = 0.0;
         if (j < d) {
             const double *p = part + j;
-            int64_t k = w;
-            for (; k + 3 * CR_WARPS < nslab; k += 4 * CR_WARPS) {
-                s0 += p[k * d];
-                s1 += p[(k + CR_WARPS) * d];
-                s2 += p[(k + 2 * CR_WARPS) * d];
-                s3 += p[(k + 3 * CR_WARPS) * d];
+            for (int64_t k0 = w; k0 < nslab; k0 += 8 * CR_WARPS) {
+                double a[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int64_t k = k0 + int64_t(i) * CR_WARPS;
+                    a[i] = k < nslab ? __ldcg(p + k * d) : 0.0;
+                }
+                s += ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
             }
-            for (; k < nslab; k += CR_WARPS) s0 += p[k * d];
         }
-        sh[w][lane] = (s0 + s1) + (s2 + s3);
+        sh[w][lane] = s;
         __syncthreads();
         if (w == 0 && j < d) {
             double t = sh[0][lane];
@@ -400,8 +403,12 @@ static int colsum_impl(const T *X, int64_t n, int64_t d, int64_t ld, double *col
     const int64_t rb = (d + 31) / 32;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_err(e, "vmf colsum partial launch");
-    e = launch_pdl(colsum_reduce_kernel, dim3(unsigned(rb < 4096 ? rb : 4096)), dim3(32 * CR_WARPS), s,
-                   (const double *)part, nslab, d, colsum, accumulate, with_count, double(n));
+    if (nslab > 64)
+        e = launch_pdl(colsum_reduce_kernel<32>, dim3(unsigned(rb < 4096 ? rb : 4096)), dim3(32 * 32), s,
+                       (const double *)part, nslab, d, colsum, accumulate, with_count, double(n));
+    else
+        e = launch_pdl(colsum_reduce_kernel<8>, dim3(unsigned(rb < 4096 ? rb : 4096)), dim3(32 * 8), s,
+                       (const double *)part, nslab, d, colsum, accumulate, with_count, double(n));
     g_launches.fetch_add(2, std::memory_order_relaxed);
     return cuda_err(e, "vmf colsum reduce launch");
 }
