@@ -81,7 +81,7 @@ constexpr int BIN_SLOW = 7;           // out-of-range / special inputs (slow_eva
 #define B200_PLOOP 1                  // 1: the unpadded evaluation loop runs on the slot index (0: element counter)
 #endif
 #ifndef B200_IFCHAIN
-#define B200_IFCHAIN 0                // 1: fused pass dispatches the cheap bins by compares
+#define B200_IFCHAIN 1                // 1: fused pass dispatches the cheap bins by compares (0: jump table only)
 #endif
 
 std::atomic<int64_t> g_launches{0};
