@@ -80,6 +80,9 @@ constexpr int BIN_SLOW = 7;           // out-of-range / special inputs (slow_eva
 #ifndef B200_PLOOP
 #define B200_PLOOP 1                  // 1: the unpadded evaluation loop runs on the slot index (0: element counter)
 #endif
+#ifndef B200_IFCHAIN1
+#define B200_IFCHAIN1 1               // 1: the single-function kernels dispatch mu, U6, U8 by compares (extending the chain to U10/U13 measured slower)
+#endif
 #ifndef B200_IFCHAIN
 #define B200_IFCHAIN 1                // 1: fused pass dispatches the cheap bins by compares (0: jump table only)
 #endif
@@ -163,6 +166,18 @@ template <typename T, int FN>
 __device__ __forceinline__ T eval_bin(int bin, T v, T x, uint32_t tab) {
 #ifdef B200_EVAL_NOP
     if (bin != BIN_SLOW) return v + x;   // experiment only: measures the tile machinery alone
+#endif
+#if B200_IFCHAIN1
+    // the cheap bins by compare-and-branch (chunk-uniform after the sort), then the jump table
+    if (FN == FN_I) {
+        if (bin == E_MU) return log_bessel_mu<T, false, false>(v, x, tab);
+        if (bin == E_UA) return log_bessel_u<T, false, KUs<T>::A, false>(v, x, tab);
+        if (bin == E_UB) return log_bessel_u<T, false, KUs<T>::B, false>(v, x, tab);
+    } else {
+        if (bin == E_MU) return log_bessel_mu<T, true, false>(fabs(v), x, tab);
+        if (bin == E_UA) return log_bessel_u<T, true, KUs<T>::A, false>(fabs(v), x, tab);
+        if (bin == E_UB) return log_bessel_u<T, true, KUs<T>::B, false>(fabs(v), x, tab);
+    }
 #endif
     if (FN == FN_I) {
         switch (bin) {
