@@ -357,7 +357,8 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 #ifndef B200_PAD
 #define B200_PAD 1           // 1: f64 fused pass: sort keys costliest first, bins padded to 32-slot chunks
 #endif
-// slots of the sorted order: TILE, plus up to 7 * 31 padding slots (B200_PAD)
+// slots of the sorted order: TILE, plus up to 8 * 31 = 248 padding slots (B200_PAD: every
+// one of the 8 keys rounded up to a multiple of 32)
 template <typename T> constexpr int idx_slots() { return TileOf<T>::tile + (B200_PAD && sizeof(T) == 8 ? 256 : 0); }
 template <typename T, int FN>
 constexpr int smem_bytes() { return 4 * TileOf<T>::tile * int(sizeof(T)) + idx_slots<T>() * 2; }   // stage[2][2][TILE] + idx
@@ -592,7 +593,7 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
             // 3. evaluate the 32-slot chunks of the sorted order, dealt to the warps in
             //    snake order (w, 15 - w, 16 + w, 31 - w, ...): the costliest chunks come
             //    first and each round of eight runs opposite to the previous one.  A padded
-            //    order spans up to TILE + 7 * 31 slots; its padding slots (0xFFFF) are skipped.
+            //    order spans up to TILE + 8 * 31 slots; its padding slots (0xFFFF) are skipped.
             //    On slot indices p = 32 c + lane the snake step needs neither the warp nor
             //    the lane: c -> c ^ 15 (16m + w -> 16m + 15 - w) then c -> (c ^ 15) + 16,
             //    i.e. p -> (p ^ 480) + ((p & 256) << 1), starting at p = tid (no SR_TID
