@@ -8,14 +8,21 @@
 //      8-byte-aligned pointers);
 //   1. every thread classifies its elements (Algorithm 1 with the GPU branch
 //      set plus cost sub-bins, integer predicates on IEEE high words);
-//   2. an in-CTA counting sort of the element indices by bin (packed 8-bit
-//      counters, warp-shuffle scans) -- the paper's "sort the input elements
-//      based on which expression is used" (§4.3) done per tile in
-//      shared memory instead of as a global sort, so no extra HBM pass;
-//   3. every warp evaluates 32 consecutive sorted slots (warp-uniform method
-//      except at <= 7 bin boundaries per tile), gathering (v, x) from the stage
-//      and writing the results in tile order;
+//   2. an in-CTA counting sort of the element indices by bin (4-bit per-thread
+//      counters widened to 8-bit warp fields, warp-shuffle scans) -- the paper's
+//      "sort the input elements based on which expression is used" (§4.3, line
+//      391) done per tile in shared memory instead of as a global sort, so no
+//      extra HBM pass; a tile whose elements share one bin skips it;
+//   3. every warp evaluates 32-slot chunks of the sorted order, gathering (v, x)
+//      from the stage and writing the results over them.  The f64 fused pass
+//      sorts costliest-first, pads every bin of a mixed tile to whole chunks (no
+//      chunk runs two methods) and deals the chunks to the warps in snake order;
+//      the other kernels keep the dense order (warp-uniform except at <= 7 bin
+//      boundaries per tile) dealt round-robin;
 //   4. one thread stores the results with a bulk copy.
+// The loops address the stage, the slot words and the log table by 32-bit shared
+// addresses computed once (sm_100a shared addresses carry the CTA's
+// cluster rank, which ptxas otherwise re-derives per access).
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
