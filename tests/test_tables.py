@@ -79,8 +79,10 @@ def test_miller_step_counts_in_kernel_source():
 
     src = open(os.path.join(os.path.dirname(gen_tables.__file__), "csrc", "bessel_math.cuh")).read()
     num = r"T\(([\d.]+)\)"
-    m = re.search(r"const int M = sizeof\(T\) == 8 \? int\(fmin\(" + num + r" \+ x, fma\(" + num + r", x, " + num
-                  + r"\)\)\) \+ 1\s*: int\(fmin\(" + num + r" \+ x, fma\(" + num + r", x, " + num + r"\)\)\) \+ 1;", src)
+    # M(x) = the step count rounded up to a multiple of 4 (four steps per loop trip)
+    m = re.search(r"const int M = \(\(sizeof\(T\) == 8 \? int\(fmin\(" + num + r" \+ x, fma\(" + num + r", x, "
+                  + num + r"\)\)\) \+ 1\s*: int\(fmin\(" + num + r" \+ x, fma\(" + num + r", x, " + num
+                  + r"\)\)\) \+ 1\) \+ 3\) & ~3;", src)
     assert m, "M(x) expression not found in log_ivkv_trap"
     a64, b64, c64, a32, b32, c32 = (float(g) for g in m.groups())
     L = np.longdouble
@@ -95,8 +97,8 @@ def test_miller_step_counts_in_kernel_source():
 
     xs = [1e-6, 1e-3, 0.3, 1.0, 2.0, 2.5, 4.9, 8.9, 13.0, 19.7, 25.0, 30.0]
     for x in xs:
-        m64 = int(min(a64 + x, b64 * x + c64)) + 1
-        m32 = int(min(a32 + x, b32 * x + c32)) + 1
+        m64 = (int(min(a64 + x, b64 * x + c64)) + 1 + 3) & ~3
+        m32 = (int(min(a32 + x, b32 * x + c32)) + 1 + 3) & ~3
         for v in (0.0, 0.5, 1.0, 4.2, 8.0, 12.69):
             ref = ratio(v, x, 120)
             if x >= 1e-3:
