@@ -81,6 +81,9 @@ constexpr int BIN_SLOW = 7;           // out-of-range / special inputs (slow_eva
 #ifndef B200_SADDR2
 #define B200_SADDR2 1                 // 1: the same in the other kernels' evaluation loop
 #endif
+#ifndef B200_HOMOSKIP
+#define B200_HOMOSKIP 1               // 1: homogeneous tiles skip the padded-base arithmetic (unused there)
+#endif
 #ifndef B200_C4
 #define B200_C4 1                     // 1: 4-bit per-thread bin counters, widened once per thread (0: 64-bit shifts)
 #endif
@@ -554,6 +557,11 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
             constexpr uint64_t F32 = 0xFFE0FFE0FFE0FFE0ull;
             uint64_t blo, bhi;
             if constexpr (PADK) {
+#if B200_HOMOSKIP
+              if (homo) {
+                blo = bhi = 0;                                                     // unused: no scatter
+              } else {
+#endif
                 // (a homogeneous tile computes the padded bases too and does not use them)
                 const uint64_t qlo = (tlo + 31 * ONES) & F32, qhi = (thi + 31 * ONES) & F32;
                 const uint64_t tp = qlo * ONES;
@@ -566,6 +574,9 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
                 const int kc = int(((warp < 4 ? tlo : thi) >> sh) & 0xFFFFull);
                 const int g = kb + kc + lane;
                 if (!homo && g < kb + ((kc + 31) & ~31)) s_idx[g] = uint16_t(0xFFFF);
+#if B200_HOMOSKIP
+              }
+#endif
             } else {
                 const uint64_t tp = tlo * ONES;
                 blo = tp - tlo;                                                    // bases of bins 0..3
