@@ -84,6 +84,9 @@ constexpr int BIN_SLOW = 7;           // out-of-range / special inputs (slow_eva
 #ifndef B200_HOMOSKIP
 #define B200_HOMOSKIP 1               // 1: homogeneous tiles skip the padded-base arithmetic (unused there)
 #endif
+#ifndef B200_REDUX
+#define B200_REDUX 1                  // 1: warp totals by REDUX; the per-thread scan only for mixed tiles (0: scan always)
+#endif
 #ifndef B200_C4
 #define B200_C4 1                     // 1: 4-bit per-thread bin counters, widened once per thread (0: 64-bit shifts)
 #endif
@@ -512,6 +515,17 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
         }
 #endif
 #endif
+#if B200_REDUX
+        // 2. per-warp totals (8-bit fields: <= 32 * 7 per key, no carries between fields)
+        //    by two 32-bit REDUX sums; the per-thread warp scan is needed only by the
+        //    scatter of a mixed tile (below)
+        {
+            const uint32_t tl = __reduce_add_sync(0xffffffffu, uint32_t(c8));
+            const uint32_t th = __reduce_add_sync(0xffffffffu, uint32_t(c8 >> 32));
+            if (lane == 0) s_wtot[warp] = (uint64_t(th) << 32) | tl;
+        }
+        __syncthreads();
+#else
         // 2. warp-inclusive scan of the packed counts, per-warp totals to smem
         uint64_t incl = c8;
 #pragma unroll
@@ -521,6 +535,7 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
         }
         if (lane == 31) s_wtot[warp] = incl;
         __syncthreads();
+#endif
         uint64_t plo = 0, phi = 0;
         int homo = 0;                // tile-homogeneous: 1 + its sort key (CTA-uniform)
         int nchunk = 0;              // B200_PAD: 32-slot chunks of the padded sorted order
@@ -582,11 +597,23 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
                 blo = tp - tlo;                                                    // bases of bins 0..3
                 bhi = thi * ONES - thi + (tp >> 48) * ONES;                        // bases of bins 4..7
             }
-            const uint64_t wlo = shfl64(blo + ilo - lo, warp), whi = shfl64(bhi + ihi - hi, warp);
-            // this thread's first slot per bin: warp offset + warp-exclusive count
-            const uint64_t ex8 = incl - c8;
-            plo = wlo + widen_lo(ex8);
-            phi = whi + widen_hi(ex8);
+#if B200_REDUX
+            if (!homo) {   // CTA-uniform: full-warp shuffles below
+                uint64_t incl = c8;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint64_t y = shfl_up64(incl, o);
+                    if (lane >= o) incl += y;
+                }
+#else
+            {
+#endif
+                const uint64_t wlo = shfl64(blo + ilo - lo, warp), whi = shfl64(bhi + ihi - hi, warp);
+                // this thread's first slot per bin: warp offset + warp-exclusive count
+                const uint64_t ex8 = incl - c8;
+                plo = wlo + widen_lo(ex8);
+                phi = whi + widen_hi(ex8);
+            }
         }
         if (!homo) {
 #pragma unroll
