@@ -131,7 +131,11 @@ int b200_log_ivkv_f64_host(const double *v_h, const double *x_h, double *out_i_h
  *   both the column sums and the global row count.  Deterministic for a given
  *   (n, d, device).  Scratch: the per-slab partials use a library-owned device
  *   buffer per (device, stream), grown on demand and kept for the process;
- *   concurrent calls on different streams or host threads are safe.
+ *   concurrent calls on different streams or host threads are safe.  A call
+ *   on a stream that has not used the library yet allocates that buffer
+ *   (cudaMalloc): before capturing into a CUDA graph, make one call on the
+ *   capture stream.  The partial -> reduce -> fit kernels are chained by
+ *   programmatic dependent launch (captured as programmatic graph edges).
  *   Errors: n < 0, d < 0, ld < d, NULL X with n > 0, NULL colsum_d.
  *
  * b200_vmf_fit_from_colsum: given the global column sum (d doubles) and the
