@@ -87,6 +87,9 @@ constexpr int BIN_SLOW = 7;           // out-of-range / special inputs (slow_eva
 #ifndef B200_REDUX
 #define B200_REDUX 1                  // 1: warp totals by REDUX; the per-thread scan only for mixed tiles (0: scan always)
 #endif
+#ifndef B200_FULLTILE
+#define B200_FULLTILE 1               // 1: full tiles classify without per-element bound checks
+#endif
 #ifndef B200_C4
 #define B200_C4 1                     // 1: 4-bit per-thread bin counters, widened once per thread (0: 64-bit shifts)
 #endif
@@ -491,6 +494,16 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
         // element; widened once per thread to the 8-bit fields of the warp scan: the even
         // keys' nibbles go to bytes 0, 2, 4, 6 and the odd keys' to bytes 1, 3, 5, 7
         uint32_t c4 = 0;
+#if B200_FULLTILE
+        if (rem == TILE) {                         // every tile but the last: no bound checks
+#pragma unroll
+            for (int i = 0; i < ITEMS; ++i) {
+                const int j = tid + i * TPB;
+                lb[i] = bin_of<T, FN>(sv[j], sx[j]);
+                c4 += 1u << (PADK ? 28 - 4 * lb[i] : 4 * lb[i]);
+            }
+        } else
+#endif
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
             const int j = tid + i * TPB;
