@@ -73,6 +73,12 @@ def run(names, n=20_000_000, reps=5):
         v = torch.empty(n, dtype=torch.float64, device=dev).uniform_(v0, v1, generator=g)
         xx = torch.empty(n, dtype=torch.float64, device=dev).uniform_(x0, x1, generator=g)
         sets[name] = (v, xx)
+    # divergence diagnostics: the fallback sets with the same pairs ordered by x (the trapezoid
+    # node count and Miller length follow x), so every warp sees nearly equal trip counts
+    for name in ("fb_a", "fb_b"):
+        v, xx = sets[name]
+        xs, perm = torch.sort(xx)
+        sets[name + "_xsorted"] = (v[perm].contiguous(), xs.contiguous())
     s = torch.cuda.current_stream(dev).cuda_stream
     res = {}
     for sname, (v, xx) in sets.items():
