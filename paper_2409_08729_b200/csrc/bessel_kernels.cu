@@ -119,6 +119,26 @@ int cuda_err(cudaError_t e, const char *where) {
 // Function ids
 enum : int { FN_I = 0, FN_K = 1, FN_K_PAPER = 2, FN_IK = 3 };   // FN_IK: both, one pass
 
+#ifndef B200_BLKMAP
+#define B200_BLKMAP 1        // 1: a thread bins ITEMS consecutive elements (odd ITEMS; see elem())
+#endif
+#ifndef B200_SB
+#define B200_SB 1            // 1: f64 fused pass: ONE stage buffer of B200_SB_ITEMS per thread
+#endif
+#ifndef B200_SB_ITEMS
+#define B200_SB_ITEMS 11     // 2816 pairs: 4 CTAs of 57.9 KB still fit the SM's 228 KB
+#endif
+// Tile shape of one kernel: double-buffered TileOf tiles, or (B200_SB, f64 fused pass) a
+// single buffer of a larger tile -- more chunks per warp between two barriers; the load of
+// the next tile is then exposed to this CTA and hidden by the SM's other CTAs
+template <typename T, int FN> struct KTile {
+    static constexpr bool sb = B200_SB && sizeof(T) == 8 && FN == FN_IK;
+    static constexpr int nbuf = sb ? 1 : 2;
+    static constexpr int items = sb ? B200_SB_ITEMS : TileOf<T>::items;
+    static constexpr int tile = TPB * items;
+    static_assert(items <= 15 && tile <= 4096, "4-bit thread counters, 12-bit tile index");
+};
+
 // ------------------------------------------------------------------ binning
 // bins 0..6 = E_MU, E_UA, E_UB, E_UC, E_U13 (U by term count), fallback split by cost (series:
 // x <= 8 / x > 8; K: Temme series x <= 2 / trapezoid x > 2); 7 = the slow bin.
@@ -370,14 +390,20 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 //      (v, x) slots (each element is read and written by one thread only);
 //   4. (one thread) bulk store of the stage's result arrays to HBM; the
 //      buffer is reloaded only after the store has read it.
+// The f64 fused pass (KTile::sb) instead keeps ONE stage of 2816 pairs and loads the
+// next tile after step 4: each warp then evaluates ~11 chunks between two barriers
+// instead of ~6, which halves the barrier waits of tiles mixing costly and cheap bins;
+// the exposed load is hidden by the SM's other three CTAs.
 #ifndef B200_PAD
 #define B200_PAD 1           // 1: f64 fused pass: sort keys costliest first, bins padded to 32-slot chunks
 #endif
 // slots of the sorted order: TILE, plus up to 8 * 31 = 248 padding slots (B200_PAD: every
 // one of the 8 keys rounded up to a multiple of 32)
-template <typename T> constexpr int idx_slots() { return TileOf<T>::tile + (B200_PAD && sizeof(T) == 8 ? 256 : 0); }
+template <typename T, int FN> constexpr int idx_slots() { return KTile<T, FN>::tile + (B200_PAD && sizeof(T) == 8 ? 256 : 0); }
 template <typename T, int FN>
-constexpr int smem_bytes() { return 4 * TileOf<T>::tile * int(sizeof(T)) + idx_slots<T>() * 2; }   // stage[2][2][TILE] + idx
+constexpr int smem_bytes() {   // stage[nbuf][2][TILE] + idx
+    return 2 * KTile<T, FN>::nbuf * KTile<T, FN>::tile * int(sizeof(T)) + idx_slots<T, FN>() * 2;
+}
 
 #ifndef B200_MINB32
 #define B200_MINB32 6        // CTAs per SM for the f32 kernels (40 registers; 4 and 5 measured slower)
@@ -387,7 +413,9 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
     bessel_eval_kernel(const T *__restrict__ vin, const T *__restrict__ xin, T *__restrict__ out,
                        T *__restrict__ out2, int64_t n) {
     constexpr int NOUT = FN == FN_IK ? 2 : 1;         // results per element (out, out2)
-    constexpr int ITEMS = TileOf<T>::items, TILE = TileOf<T>::tile;   // shadow the f64 defaults
+    constexpr int ITEMS = KTile<T, FN>::items, TILE = KTile<T, FN>::tile;   // shadow the f64 defaults
+    constexpr int NBUF = KTile<T, FN>::nbuf;
+    constexpr bool W16 = ITEMS > 7;                   // warp sums need 16-bit fields (> 255 per key)
     // padded, costliest-first sort order with snake chunk dealing: the f64 fused pass only
     // (measured: it gains on tiles mixing the fallback with cheap bins; the f32 and
     // single-function kernels, whose fallback is cheap, lose 2-3% to the extra work)
@@ -395,8 +423,8 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
     // dynamic shared memory (smem_bytes<T, FN>()): stage[2][2][TILE], idx[TILE]
     extern __shared__ __align__(128) unsigned char s_dyn[];
     auto s_stage = reinterpret_cast<T (*)[2][TILE]>(s_dyn);                       // [buffer][v|x][element]
-    uint16_t *s_idx = reinterpret_cast<uint16_t *>(s_dyn + 4 * TILE * sizeof(T));
-    __shared__ uint64_t s_wtot[TPB / 32];             // per-warp bin totals, 8-bit fields
+    uint16_t *s_idx = reinterpret_cast<uint16_t *>(s_dyn + 2 * NBUF * TILE * sizeof(T));
+    __shared__ uint64_t s_wtot[(W16 ? 2 : 1) * TPB / 32];   // per-warp bin totals, 8-bit (W16: 16-bit) fields
     __shared__ alignas(8) uint64_t s_bar[2];
 
     constexpr int VEC = 16 / int(sizeof(T));          // elements per 16 bytes (bulk-copy granule)
@@ -406,6 +434,14 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
     // its shared address, computed once and held where the compiler cannot re-derive it
     const uint32_t tab = opaque_u32(logtab_addr());
     auto tile_rem = [&](int64_t t) { return int(n - t * TILE < TILE ? n - t * TILE : TILE); };
+    // the tile elements a thread loads (cp.async, ragged tail), bins and scatters.  B200_BLKMAP:
+    // ITEMS consecutive elements per thread -- the scatter gives a thread's elements of one
+    // key consecutive sorted slots, so a chunk then reads and writes consecutive (v, x)
+    // words; with the strided map (tid + i TPB) those words share one bank pair (ITEMS-way
+    // conflicts).  ITEMS is odd, so the binning reads (stride ITEMS) stay conflict-free.
+    // (The single-function f64 kernels keep the strided map: with ITEMS = 6 the binning
+    // reads would conflict 4-way, and they measured no gain.)
+    auto elem = [&](int i) { return (B200_BLKMAP && (ITEMS & 1)) ? tid * ITEMS + i : tid + i * TPB; };
 
     // stage tile t into buffer (t / gridDim.x) & 1
     auto issue = [&](int64_t t, int buf) {
@@ -424,7 +460,7 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
         } else {
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
-                const int j = tid + i * TPB;
+                const int j = elem(i);
                 if (j < rem) {
                     cp_async<sizeof(T)>(&s_stage[buf][0][j], vin + t * TILE + j);
                     cp_async<sizeof(T)>(&s_stage[buf][1][j], xin + t * TILE + j);
@@ -445,12 +481,12 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
     if (blockIdx.x < ntiles) issue(blockIdx.x, 0);
     uint32_t parity[2] = {0u, 0u};
     int buf = 0;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= 1) {
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, buf ^= NBUF - 1) {
         const int64_t base = tile * TILE;
         const int rem = tile_rem(tile);
         // 0. prefetch the next tile into the other buffer (its readers finished
         //    before the last barrier of the previous tile)
-        if (tile + gridDim.x < ntiles) issue(tile + gridDim.x, buf ^ 1);
+        if (NBUF == 2 && tile + gridDim.x < ntiles) issue(tile + gridDim.x, buf ^ 1);
         // 1. wait for this tile, bin the owned elements
         T *sv = s_stage[buf][0], *sx = s_stage[buf][1];
         T *s_res[2] = {sv, sx};                    // results overwrite (v, x) of their own element
@@ -461,13 +497,13 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
             if (ra != rem) {                       // the (< VEC) elements past the bulk part,
 #pragma unroll                                     // loaded by the thread that bins them
                 for (int i = 0; i < ITEMS; ++i) {
-                    const int j = tid + i * TPB;
+                    const int j = elem(i);
                     if (j >= ra && j < rem) { sv[j] = vin[base + j]; sx[j] = xin[base + j]; }
                 }
             }
         } else {
             // own copies of this tile are the older group: wait for all but the newest
-            if (tile + gridDim.x < ntiles) asm volatile("cp.async.wait_group 1;" ::: "memory");
+            if (NBUF == 2 && tile + gridDim.x < ntiles) asm volatile("cp.async.wait_group 1;" ::: "memory");
             else cp_async_wait_all();
         }
         int lb[ITEMS];
@@ -478,7 +514,7 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
         uint32_t clo = 0, chi = 0;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-            const int j = tid + i * TPB;
+            const int j = elem(i);
             lb[i] = -1;
             if (j < rem) {
                 const int b = bin_of<T, FN>(sv[j], sx[j]);
@@ -498,7 +534,7 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
         if (rem == TILE) {                         // every tile but the last: no bound checks
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
-                const int j = tid + i * TPB;
+                const int j = elem(i);
                 lb[i] = bin_of<T, FN>(sv[j], sx[j]);
                 c4 += 1u << (PADK ? 28 - 4 * lb[i] : 4 * lb[i]);
             }
@@ -506,7 +542,7 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
 #endif
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-            const int j = tid + i * TPB;
+            const int j = elem(i);
             lb[i] = -1;
             if (j < rem) {
                 lb[i] = bin_of<T, FN>(sv[j], sx[j]);
@@ -519,7 +555,7 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
         uint64_t c8 = 0;
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {
-            const int j = tid + i * TPB;
+            const int j = elem(i);
             lb[i] = -1;
             if (j < rem) {
                 lb[i] = bin_of<T, FN>(sv[j], sx[j]);
@@ -532,7 +568,18 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
         // 2. per-warp totals (8-bit fields: <= 32 * 7 per key, no carries between fields)
         //    by two 32-bit REDUX sums; the per-thread warp scan is needed only by the
         //    scatter of a mixed tile (below)
-        {
+        if constexpr (W16) {
+            // per-thread 16-bit fields (keys 0-3 | 4-7), four 32-bit REDUX sums
+            const uint64_t wl = widen_lo(c8), wh = widen_hi(c8);
+            const uint32_t a0 = __reduce_add_sync(0xffffffffu, uint32_t(wl));
+            const uint32_t a1 = __reduce_add_sync(0xffffffffu, uint32_t(wl >> 32));
+            const uint32_t a2 = __reduce_add_sync(0xffffffffu, uint32_t(wh));
+            const uint32_t a3 = __reduce_add_sync(0xffffffffu, uint32_t(wh >> 32));
+            if (lane == 0) {
+                s_wtot[2 * warp] = (uint64_t(a1) << 32) | a0;
+                s_wtot[2 * warp + 1] = (uint64_t(a3) << 32) | a2;
+            }
+        } else {
             const uint32_t tl = __reduce_add_sync(0xffffffffu, uint32_t(c8));
             const uint32_t th = __reduce_add_sync(0xffffffffu, uint32_t(c8 >> 32));
             if (lane == 0) s_wtot[warp] = (uint64_t(th) << 32) | tl;
@@ -556,8 +603,15 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
             // lanes 0..NW-1 of every warp scan the per-warp totals (16-bit fields);
             // the warp keeps the exclusive prefix of its own index
             constexpr int NW = TPB / 32;
-            const uint64_t t8 = lane < NW ? s_wtot[lane] : 0ull;
-            const uint64_t lo = widen_lo(t8), hi = widen_hi(t8);
+            uint64_t lo, hi;
+            if constexpr (W16) {
+                lo = lane < NW ? s_wtot[2 * lane] : 0ull;
+                hi = lane < NW ? s_wtot[2 * lane + 1] : 0ull;
+            } else {
+                const uint64_t t8 = lane < NW ? s_wtot[lane] : 0ull;
+                lo = widen_lo(t8);
+                hi = widen_hi(t8);
+            }
             uint64_t ilo = lo, ihi = hi;
 #pragma unroll
             for (int o = 1; o < NW; o <<= 1) {
@@ -611,7 +665,19 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
                 bhi = thi * ONES - thi + (tp >> 48) * ONES;                        // bases of bins 4..7
             }
 #if B200_REDUX
-            if (!homo) {   // CTA-uniform: full-warp shuffles below
+            if (W16 && !homo) {
+                // warp scan on the 16-bit fields (two words)
+                const uint64_t cl = widen_lo(c8), ch = widen_hi(c8);
+                uint64_t xl = cl, xh = ch;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint64_t yl = shfl_up64(xl, o), yh = shfl_up64(xh, o);
+                    if (lane >= o) { xl += yl; xh += yh; }
+                }
+                const uint64_t wlo = shfl64(blo + ilo - lo, warp), whi = shfl64(bhi + ihi - hi, warp);
+                plo = wlo + (xl - cl);
+                phi = whi + (xh - ch);
+            } else if (!homo) {   // CTA-uniform: full-warp shuffles below
                 uint64_t incl = c8;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -638,7 +704,7 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
                     const uint64_t word = kk < 4 ? plo : phi;
                     const int pos = int((word >> sh) & 0xFFFFull);
                     if (kk < 4) plo += 1ull << sh; else phi += 1ull << sh;
-                    s_idx[pos] = uint16_t((tid + i * TPB) | (b << 12));   // tile index | bin
+                    s_idx[pos] = uint16_t(elem(i) | (b << 12));   // tile index | bin
                 }
             }
             __syncthreads();
@@ -746,13 +812,17 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
         } else {
 #pragma unroll
             for (int i = 0; i < ITEMS; ++i) {
-                const int j = tid + i * TPB;
+                const int j = elem(i);
                 if (j < rem) {
                     __stcs(out + base + j, s_res[0][j]);
                     if (NOUT == 2) __stcs(out2 + base + j, s_res[NOUT - 1][j]);
                 }
             }
         }
+        // single buffer: reload it once the store has read it (bulk_wait_read in issue; the
+        // cp.async path: every thread reloads only the slots it just stored).  A ragged
+        // tile is the last one, so the per-thread tail stores above never race the reload.
+        if (NBUF == 1 && tile + gridDim.x < ntiles) issue(tile + gridDim.x, 0);
     }
     if constexpr (TMA) {
         if (tid == 0) bulk_wait_all();
@@ -1086,7 +1156,7 @@ static int launch_eval(const T *v, const T *x, T *out, int64_t n, cudaStream_t s
     }
     int sms = 0;
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
-    const int64_t ntiles = (n + TileOf<T>::tile - 1) / TileOf<T>::tile;
+    const int64_t ntiles = (n + KTile<T, FN>::tile - 1) / KTile<T, FN>::tile;
     const int64_t resident = int64_t(sms) * o;
     const int grid = int(ntiles < resident ? ntiles : resident);
     if (tma)

@@ -302,6 +302,10 @@ def test_fused_ivkv_against_oracle(B, case):
     assert oracle.rel_err(gk[ok], rk).max() <= TOL64
 
 
+# pairs per tile of the f64 fused pass: KTile<double, FN_IK>::tile = TPB * B200_SB_ITEMS
+# (bessel_kernels.cu; tests/test_tile_logic.py checks the source against this value)
+FUSED_TILE = 256 * 11
+
 # one (v, x) box per evaluation bin of the fused pass (R12/R13, Table 1 predicates)
 _BIN_BOXES = {
     "mu": ((0.0, 10.0), (40.0, 90.0)),
@@ -333,15 +337,15 @@ def test_fused_every_bin_in_every_tile(B):
             tv.append(rng.uniform(v0, v1, c))
             tx.append(np.exp(rng.uniform(math.log(x0), math.log(x1), c)) if nm == "slow" else rng.uniform(x0, x1, c))
         tv, tx = np.concatenate(tv), np.concatenate(tx)
-        if len(vs) < len(counts):                  # fill the full tiles to 1536 pairs with mu pairs
-            k = 1536 - tv.size
+        if len(vs) < len(counts):                  # fill the full tiles with mu pairs
+            k = FUSED_TILE - tv.size
             tv = np.concatenate([tv, rng.uniform(0.0, 10.0, k)])
             tx = np.concatenate([tx, rng.uniform(40.0, 90.0, k)])
         perm = rng.permutation(tv.size)
         vs.append(tv[perm])
         xs.append(tx[perm])
     v, x = np.concatenate(vs), np.concatenate(xs)
-    assert v.size == 5 * 1536 + 72
+    assert v.size == 5 * FUSED_TILE + 72
     gi, gk = _run_ivkv(B, v, x)
     assert np.all(np.isfinite(gi)) and np.all(np.isfinite(gk))
     ri, rk = oracle.log_iv(v, x), oracle.log_kv(v, x)

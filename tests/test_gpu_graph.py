@@ -25,7 +25,7 @@ def B():
 
 def test_capture_and_replay_fused_eval_and_vmf_fit(B):
     dev = torch.device("cuda:0")
-    n = 3 * 1536 + 77                                  # several tiles and a ragged tail
+    n = 3 * 2816 + 77                                  # several fused-pass tiles and a ragged tail
     v0, x0 = workloads.bench_grid(n // 11 + 1, seed=5, device=dev)
     v = v0[:n].contiguous()
     x = x0[:n].contiguous()
