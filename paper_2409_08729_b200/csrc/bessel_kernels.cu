@@ -123,16 +123,16 @@ enum : int { FN_I = 0, FN_K = 1, FN_K_PAPER = 2, FN_IK = 3 };   // FN_IK: both, 
 #define B200_BLKMAP 1        // 1: a thread bins ITEMS consecutive elements (odd ITEMS; see elem())
 #endif
 #ifndef B200_SB
-#define B200_SB 1            // 1: f64 fused pass: ONE stage buffer of B200_SB_ITEMS per thread
+#define B200_SB 1            // 1: f64 kernels: ONE stage buffer of B200_SB_ITEMS per thread
 #endif
 #ifndef B200_SB_ITEMS
 #define B200_SB_ITEMS 11     // 2816 pairs: 4 CTAs of 57.9 KB still fit the SM's 228 KB
 #endif
-// Tile shape of one kernel: double-buffered TileOf tiles, or (B200_SB, f64 fused pass) a
+// Tile shape of one kernel: double-buffered TileOf tiles, or (B200_SB, the f64 kernels) a
 // single buffer of a larger tile -- more chunks per warp between two barriers; the load of
 // the next tile is then exposed to this CTA and hidden by the SM's other CTAs
 template <typename T, int FN> struct KTile {
-    static constexpr bool sb = B200_SB && sizeof(T) == 8 && FN == FN_IK;
+    static constexpr bool sb = B200_SB && sizeof(T) == 8;
     static constexpr int nbuf = sb ? 1 : 2;
     static constexpr int items = sb ? B200_SB_ITEMS : TileOf<T>::items;
     static constexpr int tile = TPB * items;
@@ -390,7 +390,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 //      (v, x) slots (each element is read and written by one thread only);
 //   4. (one thread) bulk store of the stage's result arrays to HBM; the
 //      buffer is reloaded only after the store has read it.
-// The f64 fused pass (KTile::sb) instead keeps ONE stage of 2816 pairs and loads the
+// The f64 kernels (KTile::sb) instead keep ONE stage of 2816 pairs and load the
 // next tile after step 4: each warp then evaluates ~11 chunks between two barriers
 // instead of ~6, which halves the barrier waits of tiles mixing costly and cheap bins;
 // the exposed load is hidden by the SM's other three CTAs.
@@ -439,8 +439,8 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
     // key consecutive sorted slots, so a chunk then reads and writes consecutive (v, x)
     // words; with the strided map (tid + i TPB) those words share one bank pair (ITEMS-way
     // conflicts).  ITEMS is odd, so the binning reads (stride ITEMS) stay conflict-free.
-    // (The single-function f64 kernels keep the strided map: with ITEMS = 6 the binning
-    // reads would conflict 4-way, and they measured no gain.)
+    // (An even ITEMS keeps the strided map: with ITEMS = 6 the binning reads would
+    // conflict 4-way.)
     auto elem = [&](int i) { return (B200_BLKMAP && (ITEMS & 1)) ? tid * ITEMS + i : tid + i * TPB; };
 
     // stage tile t into buffer (t / gridDim.x) & 1
