@@ -122,6 +122,9 @@ enum : int { FN_I = 0, FN_K = 1, FN_K_PAPER = 2, FN_IK = 3 };   // FN_IK: both, 
 #ifndef B200_BLKMAP
 #define B200_BLKMAP 1        // 1: a thread bins ITEMS consecutive elements (odd ITEMS; see elem())
 #endif
+#ifndef B200_SB_ITEMS32
+#define B200_SB_ITEMS32 11   // > 0: the f32 kernels on one stage of this many pairs per thread
+#endif
 #ifndef B200_SB
 #define B200_SB 1            // 1: f64 kernels: ONE stage buffer of B200_SB_ITEMS per thread
 #endif
@@ -132,9 +135,9 @@ enum : int { FN_I = 0, FN_K = 1, FN_K_PAPER = 2, FN_IK = 3 };   // FN_IK: both, 
 // single buffer of a larger tile -- more chunks per warp between two barriers; the load of
 // the next tile is then exposed to this CTA and hidden by the SM's other CTAs
 template <typename T, int FN> struct KTile {
-    static constexpr bool sb = B200_SB && sizeof(T) == 8;
+    static constexpr bool sb = B200_SB && (sizeof(T) == 8 || B200_SB_ITEMS32 > 0);
     static constexpr int nbuf = sb ? 1 : 2;
-    static constexpr int items = sb ? B200_SB_ITEMS : TileOf<T>::items;
+    static constexpr int items = !sb ? TileOf<T>::items : sizeof(T) == 8 ? B200_SB_ITEMS : B200_SB_ITEMS32;
     static constexpr int tile = TPB * items;
     static_assert(items <= 15 && tile <= 4096, "4-bit thread counters, 12-bit tile index");
 };
