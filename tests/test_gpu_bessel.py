@@ -390,6 +390,27 @@ def test_unaligned_pointers_use_the_cp_async_path(B, dtype):
         assert e.max() <= TOL64
 
 
+@pytest.mark.parametrize("dtype", [torch.float64, torch.float32])
+def test_unaligned_pointers_over_several_waves(B, dtype):
+    """More tiles than resident CTAs (148 SMs x 4-6 CTAs x 2816 pairs), so every CTA
+    reloads its single stage: the cp.async path (unaligned views) must give the same
+    bits as the bulk-copy path, for all three entry points and a ragged last tile."""
+    n = 2 * 148 * 6 * FUSED_TILE + 1235
+    v, x = workloads.bench_grid(n // 11 + 1, seed=45, device="cuda:0", dtype=dtype)
+    v, x = v[:n].contiguous(), x[:n].contiguous()
+    vt = torch.empty(n + 1, dtype=dtype, device="cuda:0")
+    xt = torch.empty(n + 1, dtype=dtype, device="cuda:0")
+    vt[1:].copy_(v)
+    xt[1:].copy_(x)
+    va, xa = vt[1:], xt[1:]
+    assert va.data_ptr() % 16 != 0
+    for fn in (B.log_iv, B.log_kv):
+        assert torch.equal(fn(va, xa), fn(v, x))
+    gi, gk = B.log_ivkv(va, xa)
+    ri, rk = B.log_ivkv(v, x)
+    assert torch.equal(gi, ri) and torch.equal(gk, rk)
+
+
 def test_tile_tails_against_separate_sizes(B):
     """Every tail length of the last tile (bulk part + < 2 leftover elements)."""
     v, x = workloads.bench_grid_numpy(400, seed=41)
