@@ -712,8 +712,9 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
             }
             __syncthreads();
         }
-        // a homogeneous tile needs no sort: every thread evaluates the elements it binned
-        // (slot p = element p), so no thread reads another's writes before the next barrier
+        // a homogeneous tile needs no sort: slot p = element p.  Its binning reads all precede
+        // the barrier after the warp totals, and each element is then read and overwritten
+        // by the one thread that evaluates its slot
         static_assert(!PADK || TPB / 32 == 8, "one warp per sort key fills that key's padding");
         const int hw = (PADK ? 7 - (homo - 1) : homo - 1) << 12;   // the tile's one bin (PADK: 7 - key)
         if constexpr (PADK) {
