@@ -171,7 +171,9 @@ __device__ __forceinline__ int bin_of(T v, T x) {
     const uint32_t hv = hvs & 0x7FFFFFFFu;
     // x outside the range (or <= 0, NaN), |v| above it (inf, NaN), v < 0 for I (-0.0 is
     // handled there): one predicate and a final select, no early-return branches
-    const bool slow = (hx - LO > HI - LO) | (hv > HI) | ((FN == FN_I || FN == FN_IK) & (hvs != hv));
+    // I (alone or fused) needs v >= 0: a set sign bit puts the raw high word above HI, so
+    // one unsigned compare covers |v| > range, NaN, v < 0 and -0.0 (K takes |v|)
+    const bool slow = (hx - LO > HI - LO) | ((FN == FN_I || FN == FN_IK) ? hvs > HI : hv > HI);
     int e;
     if constexpr (sizeof(T) == 8)
         e = select_eval_hw(fabs(v), x, hv, hx, (FN == FN_I) ? B200_HW_X8 : B200_HW_X2);
@@ -452,12 +454,24 @@ __global__ void __launch_bounds__(TPB, sizeof(T) == 4 ? B200_MINB32 : FN == FN_I
         if constexpr (TMA) {
             if (tid == 0) {
                 const int ra = rem & ~(VEC - 1);                  // bulk part (multiple of 16 bytes)
-                bulk_wait_read();                                 // this buffer's results (2 tiles ago) are out
-                fence_proxy_async();
-                mbar_expect_tx(&s_bar[buf], uint32_t(2 * ra * sizeof(T)));
-                if (ra > 0) {
-                    bulk_load(s_stage[buf][0], vin + t * TILE, uint32_t(ra * sizeof(T)), &s_bar[buf]);
-                    bulk_load(s_stage[buf][1], xin + t * TILE, uint32_t(ra * sizeof(T)), &s_bar[buf]);
+                if (NBUF == 1 && NOUT == 2) {
+                    // the v half is free once the first store (out, from the v slots) has read
+                    // it; the x half waits for the second
+                    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                    fence_proxy_async();
+                    mbar_expect_tx(&s_bar[buf], uint32_t(2 * ra * sizeof(T)));
+                    if (ra > 0) bulk_load(s_stage[buf][0], vin + t * TILE, uint32_t(ra * sizeof(T)), &s_bar[buf]);
+                    bulk_wait_read();
+                    fence_proxy_async();
+                    if (ra > 0) bulk_load(s_stage[buf][1], xin + t * TILE, uint32_t(ra * sizeof(T)), &s_bar[buf]);
+                } else {
+                    bulk_wait_read();                             // this buffer's results are out
+                    fence_proxy_async();
+                    mbar_expect_tx(&s_bar[buf], uint32_t(2 * ra * sizeof(T)));
+                    if (ra > 0) {
+                        bulk_load(s_stage[buf][0], vin + t * TILE, uint32_t(ra * sizeof(T)), &s_bar[buf]);
+                        bulk_load(s_stage[buf][1], xin + t * TILE, uint32_t(ra * sizeof(T)), &s_bar[buf]);
+                    }
                 }
             }
         } else {
