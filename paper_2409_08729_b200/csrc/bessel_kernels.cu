@@ -126,12 +126,12 @@ enum : int { FN_I = 0, FN_K = 1, FN_K_PAPER = 2, FN_IK = 3 };   // FN_IK: both, 
 #define B200_SB_ITEMS32 11   // > 0: the f32 kernels on one stage of this many pairs per thread
 #endif
 #ifndef B200_SB
-#define B200_SB 1            // 1: f64 kernels: ONE stage buffer of B200_SB_ITEMS per thread
+#define B200_SB 1            // 1: ONE stage buffer per CTA (f64: B200_SB_ITEMS, f32: B200_SB_ITEMS32 per thread)
 #endif
 #ifndef B200_SB_ITEMS
-#define B200_SB_ITEMS 11     // 2816 pairs: 4 CTAs of 57.9 KB still fit the SM's 228 KB
+#define B200_SB_ITEMS 11     // 2816 pairs: 4 CTAs of 56.3 KB (+ 1 KB reserved each) fit the SM's 228 KB
 #endif
-// Tile shape of one kernel: double-buffered TileOf tiles, or (B200_SB, the f64 kernels) a
+// Tile shape of one kernel: double-buffered TileOf tiles, or (B200_SB) a
 // single buffer of a larger tile -- more chunks per warp between two barriers; the load of
 // the next tile is then exposed to this CTA and hidden by the SM's other CTAs
 template <typename T, int FN> struct KTile {
