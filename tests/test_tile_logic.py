@@ -14,6 +14,7 @@ here exactly as the kernel evaluates them, and checked against their plain defin
     ITEMS, and the strided map's ITEMS-way conflicts in a sorted chunk.
 No GPU needed.
 """
+import math
 import os
 import random
 import re
@@ -158,3 +159,33 @@ def test_fused_tile_constant_matches_kernel_source():
     assert macro("B200_SB") == 1 and macro("B200_TPB") == 256
     from test_gpu_bessel import FUSED_TILE
     assert FUSED_TILE == macro("B200_TPB") * macro("B200_SB_ITEMS")
+
+
+def _macro_hex(name):
+    src = open(os.path.join(os.path.dirname(__file__), "..", "paper_2409_08729_b200", "csrc", "tables.h")).read()
+    return int(re.search(r"#define %s (0x[0-9A-Fa-f]+)u" % name, src).group(1), 16)
+
+
+def test_slow_bin_order_test_folds_the_sign():
+    """bin_of for log I and the fused pass tests the order with one unsigned compare of the
+    raw high word, hvs > HI; it must equal the earlier three-part test
+    hv > HI or hvs != hv (|v| above the range, NaN / inf, v < 0, -0.0), hv = hvs & 0x7FFFFFFF,
+    for every double (f64 high words) and every float (f32 bit patterns)."""
+    import struct
+    rng = random.Random(5)
+    specials = [0.0, -0.0, 1.0, -1.0, 1e140, 1.0000000001e140, -1e140, 9.99e139, float("inf"),
+                float("-inf"), float("nan"), -float("nan"), 5e-324, -5e-324, 1e-300, 1e300, -1e300]
+    for hi_name, fmt, width in (("B200_HW_HI", "<d", 64), ("B200_F32_HI32", "<f", 32)):
+        HI = _macro_hex(hi_name)
+        vals = specials + [rng.choice([-1, 1]) * 10 ** rng.uniform(-307, 307) for _ in range(5000)]
+        for v in vals:
+            try:
+                bits = int.from_bytes(struct.pack(fmt, v), "little")
+            except OverflowError:                       # beyond the float range: +-inf
+                bits = int.from_bytes(struct.pack(fmt, math.copysign(float("inf"), v)), "little")
+            hvs = bits >> 32 if width == 64 else bits
+            hv = hvs & 0x7FFFFFFF
+            assert (hvs > HI) == (hv > HI or hvs != hv), (v, hex(hvs))
+        for hvs in [rng.getrandbits(32) for _ in range(20000)] + [HI, HI + 1, HI | 0x80000000, 0x80000000]:
+            hv = hvs & 0x7FFFFFFF
+            assert (hvs > HI) == (hv > HI or hvs != hv)
