@@ -697,6 +697,30 @@ def test_pure_relative_accuracy_where_log_iv_is_small(B):
     assert np.all(np.abs(gi[~nz]) <= 1e-300)
 
 
+def test_mu_corner_cancellation(B):
+    """The corner of the mu region (x just above 30, v up to 15.39: Table 1) is where the
+    series for I alternates and cancels most (terms up to ~9 summing to ~0.02).  f32 must
+    stay inside its bar there for both entry points -- the fused pass once summed S_I as
+    E - O in float and reached 1.06e-5 (profiles/r165) -- and f64 inside its own."""
+    rng = np.random.default_rng(47)
+    n = 100_000
+    v = rng.uniform(12.0, 15.39, n)
+    x = rng.uniform(30.0, 32.0, n)
+    for dtype, tol in ((torch.float32, TOL32), (torch.float64, TOL64)):
+        if dtype == torch.float32:
+            vv = v.astype(np.float32).astype(np.float64)
+            xx = x.astype(np.float32).astype(np.float64)
+        else:
+            vv, xx = v, x
+        ri, rk = oracle.log_iv(vv, xx), oracle.log_kv(vv, xx)
+        gi, gk = _run_ivkv(B, vv, xx, dtype)
+        si = _run(B, "iv", vv, xx, dtype)
+        for got, ref, what in ((gi, ri, "fused I"), (gk, rk, "fused K"), (si, ri, "log_iv")):
+            e = oracle.rel_err(got, ref)
+            i = int(np.argmax(e))
+            assert e[i] <= tol, f"{dtype} {what}: {e[i]:.3e} at v={vv[i]!r} x={xx[i]!r}"
+
+
 def test_fused_f32_temme_band(B):
     """f32 fused pass on 0.1 <= x <= 2, 1/2 <= v <= 12.7, where log I comes from Temme's K values
     by the Wronskian and Miller's ratio (float range: the ratio is formed before the product

@@ -31,14 +31,15 @@ def main(n=20000, seed=0, dtype=torch.float64):
         vt = torch.tensor(v, device="cuda:0", dtype=dtype)
         xt = torch.tensor(x, device="cuda:0", dtype=dtype)
         row = {}
+        refs = {"iv": oracle.log_iv(v, x), "kv": oracle.log_kv(v, x)}     # once per set
         for fn in ("iv", "kv"):
             got = (B.log_iv if fn == "iv" else B.log_kv)(vt, xt).double().cpu().numpy()
-            ref = (oracle.log_iv if fn == "iv" else oracle.log_kv)(v, x)
+            ref = refs[fn]
             e = oracle.rel_err(got, ref)
             i = int(np.argmax(e))
             row[fn] = {"max": float(e[i]), "p99": float(np.quantile(e, 0.99)), "at": [float(v[i]), float(x[i])]}
         fi, fk = B.log_ivkv(vt, xt)
-        for nm, got, ref in (("ivkv_i", fi, oracle.log_iv(v, x)), ("ivkv_k", fk, oracle.log_kv(v, x))):
+        for nm, got, ref in (("ivkv_i", fi, refs["iv"]), ("ivkv_k", fk, refs["kv"])):
             e = oracle.rel_err(got.double().cpu().numpy(), ref)
             i = int(np.argmax(e))
             row[nm] = {"max": float(e[i]), "p99": float(np.quantile(e, 0.99)), "at": [float(v[i]), float(x[i])]}
@@ -50,8 +51,9 @@ def main(n=20000, seed=0, dtype=torch.float64):
 
 
 if __name__ == "__main__":
-    # usage: python tools/accuracy_report.py [out.json] [points per set] [f32]
+    # usage: python tools/accuracy_report.py [out.json] [points per set] [f32] [seed=S]
     dt = torch.float32 if "f32" in sys.argv[3:] else torch.float64
-    r = main(int(sys.argv[2]), dtype=dt) if len(sys.argv) > 2 else main()
+    sd = [int(a[5:]) for a in sys.argv[3:] if a.startswith("seed=")]
+    r = main(int(sys.argv[2]), seed=sd[0] if sd else 0, dtype=dt) if len(sys.argv) > 2 else main()
     if len(sys.argv) > 1:
         json.dump(r, open(sys.argv[1], "w"), indent=1)
