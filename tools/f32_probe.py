@@ -6,7 +6,7 @@ at the U13 / fallback edge and in the fallback band of log I alone.  This sample
 box with 1M points (inputs rounded to float, the oracle at those inputs) and prints
 the max error of log I, log K and the fused pass per box.
 
-  python tools/f32_probe.py [out.json] [points per box]
+  python tools/f32_probe.py [out.json] [points per box] [f64]   (f64: the f64 boxes)
 """
 import json
 import sys
@@ -32,14 +32,31 @@ def boxes(rng, n):
     yield "mu_corner", rng.uniform(10.0, 15.39, n), rng.uniform(30.0, 36.0, n)
 
 
-def main(n=1_000_000):
+def boxes64(rng, n):
+    """f64: the U13 / fallback edge, the U term-count changes at rho = 61 / 107, the edges
+    of the f64 eta band (0.03), the mu corner, U13 at small v just past x = 19.69."""
+    lv = lambda a, b: np.exp(rng.uniform(np.log(a), np.log(b), n))   # noqa: E731
+    yield "u13_fb_edge", rng.uniform(12.69, 14.0, n), rng.uniform(4.0, 12.0, n)
+    for rho in (61.0, 107.0):
+        r = rho * rng.uniform(1.0, 1.03, n)
+        th = rng.uniform(0.0, np.pi / 2, n)
+        yield f"rho{int(rho)}_edge", r * np.cos(th), r * np.sin(th)
+    v = lv(13.0, 2000.0)
+    yield "eta_edge", v, v * (Z0 + rng.choice([-1.0, 1.0], n) * rng.uniform(0.03, 0.05, n))
+    yield "mu_corner", rng.uniform(10.0, 15.39, n), rng.uniform(30.0, 36.0, n)
+    yield "u13_low_v", rng.uniform(0.7, 2.0, n), rng.uniform(19.69, 22.0, n)
+
+
+def main(n=1_000_000, f64=False):
     rng = np.random.default_rng(11)
     res = {}
-    for name, v, x in boxes(rng, n):
-        v = v.astype(np.float32).astype(np.float64)
-        x = x.astype(np.float32).astype(np.float64)
-        vt = torch.tensor(v, device="cuda:0", dtype=torch.float32)
-        xt = torch.tensor(x, device="cuda:0", dtype=torch.float32)
+    dt = torch.float64 if f64 else torch.float32
+    for name, v, x in (boxes64 if f64 else boxes)(rng, n):
+        if not f64:
+            v = v.astype(np.float32).astype(np.float64)
+            x = x.astype(np.float32).astype(np.float64)
+        vt = torch.tensor(v, device="cuda:0", dtype=dt)
+        xt = torch.tensor(x, device="cuda:0", dtype=dt)
         ri, rk = oracle.log_iv(v, x), oracle.log_kv(v, x)
         fi, fk = B.log_ivkv(vt, xt)
         row = {}
@@ -55,6 +72,6 @@ def main(n=1_000_000):
 
 
 if __name__ == "__main__":
-    r = main(int(sys.argv[2])) if len(sys.argv) > 2 else main()
+    r = main(int(sys.argv[2]), f64="f64" in sys.argv[3:]) if len(sys.argv) > 2 else main()
     if len(sys.argv) > 1:
         json.dump(r, open(sys.argv[1], "w"), indent=1)
