@@ -22,4 +22,4 @@ for dt, name in ((torch.float32, "f32"), (torch.float64, "f64")):
         row[what] = {"max": float(e[i]), "at": [float(v[i]), float(x[i])], "nonfinite": int((~np.isfinite(g)).sum())}
     out[name] = row
     print(name, row, flush=True)
-json.dump(out, open("sys.argv[1] if len(sys.argv) > 1 else "wide.json"", "w"), indent=1)
+json.dump(out, open(sys.argv[1] if len(sys.argv) > 1 else "wide.json", "w"), indent=1)
